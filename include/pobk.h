@@ -1,0 +1,169 @@
+/*
+ * pobk.h -- C ABI of libpobk.so, the B200 (sm_100a) implementation of the hot path of the
+ * preprocessed orthogonal block Kaczmarz method (POBK), arXiv 2401.00672.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (the paper's LaTeX source);
+ * readings of the paper that this library implements are listed in DESIGN.md §3 and
+ * SURVEY.md §8(c) (Z1-Z20).
+ *
+ * What the library computes (Alg 5, at row granularity):
+ *   preprocess:  P from Reverse Cuthill-McKee, A~ = P A P^T (Eq 3.1),
+ *                rows of A~ partitioned into categories of pairwise-orthogonal rows by the
+ *                first-orthogonal rule iterated to maximal classes; schedule =
+ *                Oclass categories (>= 2 rows) in ascending colour, then Nclass rows ascending.
+ *   solve:       sweeps over the schedule; each category applies the block step Eq 1.3
+ *                (P:34-37), which for pairwise-orthogonal rows collapses by Lemma 1
+ *                 into simultaneous row projections Eq 1.2:
+ *                    r_i = f~_i - a~_i . x~,  alpha_i = r_i / ||a~_i||^2,  x~ += alpha_i a~_i^T;
+ *                stop when RSE = ||x - x*|| / ||x*|| < tol or at max_sweeps; then
+ *                x = P^T x~.
+ *   residual:    ||f - A x||_2 (the fused SpMV + norm of the convergence check).
+ *
+ * Conventions (all functions):
+ *   - Every function returns pobk_status (0 = POBK_OK).  No C++ exception crosses the ABI.
+ *     On error, pobk_last_error() returns a thread-local message naming the offending item.
+ *   - Host input arrays are caller-owned, read-only and copied; the library keeps no pointer.
+ *   - Device pointers ("_dev") are caller-owned allocations on the plan's device (e.g. torch
+ *     tensors); the library never frees them.  Vectors are fp64, length m, in the USER frame.
+ *   - The plan owns every internal host and device buffer; pobk_plan_destroy frees them.
+ *   - A plan is not re-entrant: one solve at a time per plan.  Distinct plans are independent
+ *     and may be used from different host threads.
+ *   - Calls that touch the GPU set the plan's device and restore the caller's current device.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).  Calls
+ *     that return results to the host synchronise that stream before returning.
+ */
+#ifndef POBK_H_
+#define POBK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POBK_ABI_VERSION 1
+
+typedef struct pobk_plan_s* pobk_plan_t;
+typedef int32_t pobk_status;
+
+enum {
+  POBK_OK = 0,
+  POBK_ERR_ARG = 1,          /* NULL pointer, m < 1, bad option value, plan without device */
+  POBK_ERR_BAD_CSR = 2,      /* row_ptr not monotone / row_ptr[0] != 0, column out of range,
+                                columns unsorted or duplicated within a row */
+  POBK_ERR_ZERO_ROW = 3,     /* ||a_i|| = 0 after dropping explicit zeros: Eq 1.2 undefined */
+  POBK_ERR_UNSTABLE_THR = 4, /* thr > 0 and a row fails the Gershgorin guard (opts.guard = 1) */
+  POBK_ERR_CUDA = 5,         /* a CUDA runtime call failed (message names it) */
+  POBK_ERR_OOM = 6,          /* host or device allocation failed */
+  POBK_ERR_NO_DEVICE = 7     /* operation needs a device plan (device >= 0) */
+};
+
+enum { POBK_TERM_CONVERGED = 0, POBK_TERM_MAX_SWEEPS = 1, POBK_TERM_NONFINITE = 2 };
+
+enum {
+  POBK_STOP_RSE = 0,    /* RSE = ||x~ - x~*|| / ||x~*||; needs xstar */
+  POBK_STOP_RELRES = 1, /* ||f~ - A~ x~|| / ||f~|| (fused SpMV + norm every check) */
+  POBK_STOP_NONE = 2    /* run exactly max_sweeps sweeps, no check (fixed-count parity) */
+};
+
+/* Sweep kernel families.  AUTO picks by size and thr. */
+enum {
+  POBK_KERNEL_AUTO = 0,
+  POBK_KERNEL_LAUNCH = 1,    /* K1: one launch per category step, device-driven CUDA-graph loop */
+  POBK_KERNEL_WAVEFRONT = 2, /* K2: persistent tiled wavefront, x~ tile-private in shared memory */
+  POBK_KERNEL_SMEM = 3       /* K3: one CTA, whole system resident in shared memory */
+};
+
+typedef struct {
+  double thr;        /* 0 (default): structural orthogonality (disjoint supports, Z5/Z7);
+                        > 0: |cos(a_i, a_l)| < thr counts as orthogonal, categories
+                        may overlap and use the simultaneous (fp64 atomic) update */
+  int32_t reorder;   /* 1 (default): RCM; 0: identity (narrow-band matrices) */
+  int32_t kernel;    /* POBK_KERNEL_*; default AUTO */
+  int32_t tile_rows; /* K2 target rows per tile; 0 = auto */
+  int32_t guard;     /* thr > 0 only: 1 = fail with POBK_ERR_UNSTABLE_THR when some row has
+                        sum_{l in its category, l != i} |cos(a_i, a_l)| >= 1; default 0 */
+} pobk_preprocess_opts;
+
+typedef struct {
+  double tol;           /* default 1e-6; stop when value < tol (strict) */
+  int64_t max_sweeps;   /* default 500000 */
+  int32_t stop;         /* POBK_STOP_*; default POBK_STOP_RSE */
+  int32_t check_every;  /* check after every k-th sweep; default 1 (needed for +-1 parity) */
+} pobk_solve_opts;
+
+typedef struct {
+  int64_t sweeps;        /* sweeps performed by this call */
+  int32_t termination;   /* POBK_TERM_* */
+  int32_t kernel;        /* POBK_KERNEL_* actually used */
+  double final_value;    /* last checked RSE or RELRES (NaN with POBK_STOP_NONE) */
+  double solve_seconds;  /* CUDA-event time of the whole solve on `stream` (permute in .. out) */
+  double sweep_seconds;  /* CUDA-event time of the sweep kernel(s) alone */
+  int64_t launches;      /* kernels launched by this call (graph-launched nodes included) */
+} pobk_report;
+
+void pobk_preprocess_opts_default(pobk_preprocess_opts* o);
+void pobk_solve_opts_default(pobk_solve_opts* o);
+
+/* Alg 5 steps 1-4.  Validates the 0-based CSR (row_ptr int64[m+1], col int32[nnz],
+ * val fp64[nnz]; columns strictly increasing within a row), drops explicit zeros, computes the
+ * RCM permutation (George-Liu start, (degree, index) ties, components by minimum index, full
+ * reversal), the first-fit partition and schedule, and builds the device layout.
+ * device >= 0: upload to that CUDA device; device = -1: host-only plan (queries only, no solve).
+ * *out receives a new plan (NULL on error). */
+pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* col, const double* val,
+                            const pobk_preprocess_opts* opts, int device, pobk_plan_t* out);
+
+/* Sizes and preprocessing statistics; any output pointer may be NULL.  nsteps = number of
+ * schedule steps (Oclass categories + Nclass rows); bandwidths are max |i - j| before/after. */
+pobk_status pobk_plan_info(pobk_plan_t plan, int64_t* m, int64_t* nnz, int32_t* nsteps, int32_t* n_oclass,
+                           int64_t* bw_before, int64_t* bw_after, double* preprocess_seconds);
+
+/* perm[m]: the RCM permutation, perm[new] = old (Eq 3.1: f~ = P f means f~[i] = f[perm[i]]). */
+pobk_status pobk_plan_get_perm(pobk_plan_t plan, int32_t* perm);
+
+/* color[m] (first-fit colour of each RCM-frame row), cat_ptr[nsteps+1], cat_rows[m] (RCM-frame
+ * rows in schedule order).  Any pointer may be NULL. */
+pobk_status pobk_plan_get_partition(pobk_plan_t plan, int32_t* color, int32_t* cat_ptr, int32_t* cat_rows);
+
+/* The K2 tiling (for tests): ntiles, and for each RCM-frame row its tile.  Either may be NULL. */
+pobk_status pobk_plan_get_tiles(pobk_plan_t plan, int32_t* ntiles, int32_t* tile_of_row);
+
+/* Iterate from x0 = x_dev (in/out, user frame) until the stop rule; x_dev receives x = P^T x~.
+ * f_dev: right-hand side; xstar_dev: exact solution (required for POBK_STOP_RSE, else may be
+ * NULL).  Blocks until *rep is filled.  opts NULL = defaults. */
+pobk_status pobk_solve(pobk_plan_t plan, const double* f_dev, double* x_dev, const double* xstar_dev,
+                       const pobk_solve_opts* opts, void* stream, pobk_report* rep);
+
+/* Same as pobk_solve with HOST vectors: copies f, x0 (and x*) to the device, solves, copies x
+ * back (end-to-end path).  Host buffers may be pageable; pinned memory copies faster. */
+pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const double* xstar,
+                            const pobk_solve_opts* opts, void* stream, pobk_report* rep);
+
+/* nb independent systems (one plan each, same device), solved back to back on `stream`; every
+ * system stops on its own rule.  Arrays of nb device pointers; reps[nb]. */
+pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const* f_dev, double* const* x_dev,
+                             const double* const* xstar_dev, const pobk_solve_opts* opts, void* stream,
+                             pobk_report* reps);
+
+/* *out = ||f - A x||_2 in the user frame (fused SpMV + squared-norm kernel, deterministic
+ * two-level reduction).  Device vectors; result returned to the host. */
+pobk_status pobk_residual_norm(pobk_plan_t plan, const double* f_dev, const double* x_dev, void* stream,
+                               double* out);
+
+/* *out = sum_{row_begin <= i < row_end} (f_i - a_i . x)^2 over USER-frame rows (the per-rank part
+ * of a row-sharded residual; combine across ranks with an all-reduce SUM). */
+pobk_status pobk_residual_sumsq_rows(pobk_plan_t plan, int64_t row_begin, int64_t row_end, const double* f_dev,
+                                     const double* x_dev, void* stream, double* out);
+
+void pobk_plan_destroy(pobk_plan_t plan);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* pobk_last_error(void);
+
+int32_t pobk_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POBK_H_ */

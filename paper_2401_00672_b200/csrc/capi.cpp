@@ -1,0 +1,405 @@
+// The C ABI of libpobk.so (include/pobk.h): argument checking, plan construction (host
+// preprocessing + device layout), solve orchestration and reports.  No C++ exception crosses
+// the ABI; every failure becomes a pobk_status plus a thread-local message.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "plan.h"
+
+namespace pobk {
+namespace {
+
+thread_local std::string g_err;
+
+pobk_status fail(pobk_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return fail(POBK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+cudaError_t dalloc(Plan& p, T** ptr, size_t count) {
+  void* v = nullptr;
+  cudaError_t e = cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(T));
+  if (e == cudaSuccess) {
+    p.allocations.push_back(v);
+    *ptr = (T*)v;
+  }
+  return e;
+}
+
+template <typename T>
+cudaError_t upload(Plan& p, T** ptr, const T* src, size_t count) {
+  cudaError_t e = dalloc(p, ptr, count);
+  if (e == cudaSuccess && count) e = cudaMemcpy(*ptr, src, count * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+// Lanes per row: nearest power of two to half the mean row length, in [2, 32]; fixes the
+// per-row summation tree shared by all kernel families (common.cuh).
+int choose_lanes(int64_t m, int64_t nnz) {
+  const double half = 0.5 * (double)nnz / (double)m;
+  int v = 2;
+  while (v < 32 && (double)(2 * v) <= half * 1.5) v *= 2;
+  return v;
+}
+
+void destroy_plan(Plan* p) {
+  if (!p) return;
+  if (p->device >= 0) {
+    DeviceGuard g(p->device);
+    if (p->k2) k2_free(*p);
+    if (p->k1_exec) cudaGraphExecDestroy(p->k1_exec);
+    if (p->k1_graph) cudaGraphDestroy(p->k1_graph);
+    for (void* a : p->allocations) cudaFree(a);
+    if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
+    for (auto& e : p->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete static_cast<pobk_plan_s*>(p);
+}
+
+pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows) {
+  DeviceGuard g(p.device);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice(" + std::to_string(p.device) + ") failed");
+  const int64_t m = p.m;
+  // schedule-order (step-major) CSR
+  std::vector<int32_t> rp(m + 1), col(p.nnz), orig(m);
+  std::vector<double> val(p.nnz), nrm2_s(m);
+  rp[0] = 0;
+  for (int64_t s = 0; s < m; s++) {
+    const int32_t r = p.sched.rows[s];
+    const int64_t b = At.ptr[r], len = At.ptr[r + 1] - b;
+    std::memcpy(col.data() + rp[s], At.col.data() + b, len * sizeof(int32_t));
+    std::memcpy(val.data() + rp[s], At.val.data() + b, len * sizeof(double));
+    rp[s + 1] = rp[s] + (int32_t)len;
+    nrm2_s[s] = nrm2[r];
+    orig[s] = p.perm[r];
+  }
+  CUDA_TRY(upload(p, &p.A.rp, rp.data(), m + 1));
+  CUDA_TRY(upload(p, &p.A.col, col.data(), p.nnz));
+  CUDA_TRY(upload(p, &p.A.val, val.data(), p.nnz));
+  CUDA_TRY(upload(p, &p.A.nrm2, nrm2_s.data(), m));
+  CUDA_TRY(upload(p, &p.A.orig, orig.data(), m));
+  CUDA_TRY(upload(p, &p.d_perm, p.perm.data(), m));
+  p.h_step_ptr = p.sched.step_ptr;
+  p.h_overlap = p.sched.overlap;
+  CUDA_TRY(upload(p, &p.k3_step_ptr, p.h_step_ptr.data(), p.h_step_ptr.size()));
+  CUDA_TRY(upload(p, &p.k3_overlap, p.h_overlap.data(), p.h_overlap.size()));
+  int32_t max_step = 0;
+  for (int32_t k = 0; k < p.nsteps; k++) max_step = std::max(max_step, p.h_step_ptr[k + 1] - p.h_step_ptr[k]);
+  CUDA_TRY(dalloc(p, &p.d_xt, m));
+  CUDA_TRY(dalloc(p, &p.d_xst, m));
+  CUDA_TRY(dalloc(p, &p.d_fs, m));
+  CUDA_TRY(dalloc(p, &p.d_alpha, p.any_overlap ? max_step : 1));
+  CUDA_TRY(dalloc(p, &p.d_partials, kMaxReduceBlocks));
+  CUDA_TRY(dalloc(p, &p.d_ctrl, 1));
+  CUDA_TRY(cudaMemset(p.d_ctrl, 0, sizeof(Ctrl)));
+  CUDA_TRY(cudaMallocHost(&p.h_ctrl, sizeof(Ctrl)));
+  for (auto& e : p.ev) CUDA_TRY(cudaEventCreate(&e));
+
+  // kernel family: K3 when everything fits one CTA's shared memory, else the K2
+  // wavefront when its tiling is valid, else K1.  Overlapping categories (thr > 0) use K1/K3.
+  const int req = p.kernel;
+  size_t k3b = 0;
+  const bool k3ok = k3_fits(p, k3b);
+  if (k3ok) p.k3_smem = k3b;
+  std::string why;
+  if (req == POBK_KERNEL_SMEM) {
+    if (!k3ok) return fail(POBK_ERR_ARG, "kernel=SMEM requested but the system needs " + std::to_string(k3b) + " B of shared memory");
+  } else if (req == POBK_KERNEL_WAVEFRONT) {
+    if (p.any_overlap) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT does not support overlapping categories (thr > 0)");
+    if (!k2_build(p, At, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
+  } else if (req == POBK_KERNEL_AUTO) {
+    if (k3ok) p.kernel = POBK_KERNEL_SMEM;
+    else if (!p.any_overlap && m >= 65536 && k2_build(p, At, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
+    else p.kernel = POBK_KERNEL_LAUNCH;
+  }
+  return POBK_OK;
+}
+
+pobk_status solve_device(Plan& p, const double* f, double* x, const double* xstar, const pobk_solve_opts& o,
+                         cudaStream_t s, pobk_report* rep) {
+  long long launches = 0;
+  CUDA_TRY(cudaEventRecord(p.ev[0], s));
+  CUDA_TRY(launch_permute_in(p, f, x, xstar, p.d_fs, p.d_xt, o.stop == POBK_STOP_RSE ? p.d_xst : nullptr, s, launches));
+  CUDA_TRY(launch_init_ctrl(p, o, s, launches));
+  CUDA_TRY(cudaEventRecord(p.ev[1], s));
+  if (o.max_sweeps > 0) {
+    switch (p.kernel) {
+      case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
+      case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, s, launches)); break;
+      default: CUDA_TRY(k1_solve(p, s, launches)); break;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(p.ev[2], s));
+  CUDA_TRY(launch_permute_out(p, x, s, launches));
+  CUDA_TRY(cudaEventRecord(p.ev[3], s));
+  CUDA_TRY(cudaMemcpyAsync(p.h_ctrl, p.d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  float t_all = 0.f, t_sw = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&t_all, p.ev[0], p.ev[3]));
+  CUDA_TRY(cudaEventElapsedTime(&t_sw, p.ev[1], p.ev[2]));
+  const Ctrl& c = *p.h_ctrl;
+  if (p.kernel == POBK_KERNEL_LAUNCH && o.max_sweeps > 0) launches += c.sweeps * p.k1_nodes_per_sweep;
+  if (rep) {
+    rep->sweeps = o.max_sweeps > 0 ? c.sweeps : 0;
+    rep->termination = c.term;
+    rep->kernel = p.kernel;
+    rep->final_value = (o.stop == POBK_STOP_NONE) ? NAN : c.value;
+    rep->solve_seconds = t_all * 1e-3;
+    rep->sweep_seconds = t_sw * 1e-3;
+    rep->launches = launches;
+  }
+  return POBK_OK;
+}
+
+pobk_status check_solve_args(pobk_plan_t plan, const void* f, const void* x, const void* xstar, pobk_solve_opts& o,
+                             const pobk_solve_opts* opts) {
+  if (!plan) return fail(POBK_ERR_ARG, "plan is NULL");
+  if (plan->device < 0) return fail(POBK_ERR_NO_DEVICE, "plan was built with device = -1 (host-only)");
+  if (!f || !x) return fail(POBK_ERR_ARG, "f and x must be non-NULL");
+  pobk_solve_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.stop < POBK_STOP_RSE || o.stop > POBK_STOP_NONE) return fail(POBK_ERR_ARG, "opts.stop out of range");
+  if (o.stop == POBK_STOP_RSE && !xstar) return fail(POBK_ERR_ARG, "POBK_STOP_RSE needs xstar");
+  if (o.check_every < 1) return fail(POBK_ERR_ARG, "opts.check_every must be >= 1");
+  if (o.max_sweeps < 0) return fail(POBK_ERR_ARG, "opts.max_sweeps must be >= 0");
+  if (!(o.tol >= 0.0)) return fail(POBK_ERR_ARG, "opts.tol must be >= 0");
+  return POBK_OK;
+}
+
+}  // namespace
+}  // namespace pobk
+
+using namespace pobk;
+
+extern "C" {
+
+void pobk_preprocess_opts_default(pobk_preprocess_opts* o) {
+  if (!o) return;
+  o->thr = 0.0;
+  o->reorder = 1;
+  o->kernel = POBK_KERNEL_AUTO;
+  o->tile_rows = 0;
+  o->guard = 0;
+}
+
+void pobk_solve_opts_default(pobk_solve_opts* o) {
+  if (!o) return;
+  o->tol = 1e-6;
+  o->max_sweeps = 500000;
+  o->stop = POBK_STOP_RSE;
+  o->check_every = 1;
+}
+
+int32_t pobk_abi_version(void) { return POBK_ABI_VERSION; }
+
+const char* pobk_last_error(void) { return g_err.c_str(); }
+
+pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* col, const double* val,
+                            const pobk_preprocess_opts* opts, int device, pobk_plan_t* out) {
+  g_err.clear();
+  if (!out) return fail(POBK_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  pobk_preprocess_opts o;
+  pobk_preprocess_opts_default(&o);
+  if (opts) o = *opts;
+  if (!(o.thr >= 0.0 && o.thr < 1.0)) return fail(POBK_ERR_ARG, "opts.thr must be in [0, 1)");
+  if (o.kernel < POBK_KERNEL_AUTO || o.kernel > POBK_KERNEL_SMEM) return fail(POBK_ERR_ARG, "opts.kernel out of range");
+  if (device < -1) return fail(POBK_ERR_ARG, "device must be >= -1");
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    HostCSR A;
+    Error err;
+    if (!canonicalize(m, row_ptr, col, val, A, err)) return fail(err.code, err.msg);
+    Plan* p = new pobk_plan_s();
+    p->device = device;
+    p->m = m;
+    p->nnz = A.nnz();
+    p->thr = o.thr;
+    p->kernel = o.kernel;
+    p->bw_before = bandwidth(A);
+    if (o.reorder) rcm_order(A, p->perm);
+    else {
+      p->perm.resize(m);
+      for (int64_t i = 0; i < m; i++) p->perm[i] = (int32_t)i;
+    }
+    HostCSR At;
+    permute_symmetric(A, p->perm, At);
+    { HostCSR().ptr.swap(A.ptr); std::vector<int32_t>().swap(A.col); std::vector<double>().swap(A.val); }
+    p->bw_after = bandwidth(At);
+    std::vector<double> nrm2;
+    row_sqnorms(At, nrm2);
+    first_fit_colour(At, nrm2, o.thr, p->colour);
+    build_schedule(At, p->colour, o.thr > 0.0, p->sched);
+    p->nsteps = (int32_t)p->sched.step_ptr.size() - 1;
+    p->n_oclass = p->sched.n_oclass;
+    for (uint8_t v : p->sched.overlap) p->any_overlap |= (v != 0);
+    if (o.thr > 0.0 && o.guard) {
+      std::string why;
+      if (!gershgorin_guard(At, nrm2, p->colour, why)) {
+        destroy_plan(p);
+        return fail(POBK_ERR_UNSTABLE_THR, why);
+      }
+    }
+    p->V = choose_lanes(m, p->nnz);
+    if (device >= 0) {
+      pobk_status st = build_device(*p, At, nrm2, o.tile_rows);
+      if (st != POBK_OK) {
+        std::string keep = g_err;
+        destroy_plan(p);
+        g_err = keep;
+        return st;
+      }
+    } else if (p->kernel == POBK_KERNEL_AUTO) {
+      p->kernel = POBK_KERNEL_LAUNCH;
+    }
+    p->prep_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = static_cast<pobk_plan_s*>(p);
+    return POBK_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(POBK_ERR_OOM, "host allocation failed during preprocessing");
+  } catch (const std::exception& e) {
+    return fail(POBK_ERR_ARG, std::string("preprocessing failed: ") + e.what());
+  }
+}
+
+pobk_status pobk_plan_info(pobk_plan_t p, int64_t* m, int64_t* nnz, int32_t* nsteps, int32_t* n_oclass, int64_t* bw_before,
+                           int64_t* bw_after, double* prep) {
+  if (!p) return fail(POBK_ERR_ARG, "plan is NULL");
+  if (m) *m = p->m;
+  if (nnz) *nnz = p->nnz;
+  if (nsteps) *nsteps = p->nsteps;
+  if (n_oclass) *n_oclass = p->n_oclass;
+  if (bw_before) *bw_before = p->bw_before;
+  if (bw_after) *bw_after = p->bw_after;
+  if (prep) *prep = p->prep_seconds;
+  return POBK_OK;
+}
+
+pobk_status pobk_plan_get_perm(pobk_plan_t p, int32_t* perm) {
+  if (!p || !perm) return fail(POBK_ERR_ARG, "plan and perm must be non-NULL");
+  std::memcpy(perm, p->perm.data(), p->m * sizeof(int32_t));
+  return POBK_OK;
+}
+
+pobk_status pobk_plan_get_partition(pobk_plan_t p, int32_t* colour, int32_t* cat_ptr, int32_t* cat_rows) {
+  if (!p) return fail(POBK_ERR_ARG, "plan is NULL");
+  if (colour) std::memcpy(colour, p->colour.data(), p->m * sizeof(int32_t));
+  if (cat_ptr) std::memcpy(cat_ptr, p->sched.step_ptr.data(), p->sched.step_ptr.size() * sizeof(int32_t));
+  if (cat_rows) std::memcpy(cat_rows, p->sched.rows.data(), p->m * sizeof(int32_t));
+  return POBK_OK;
+}
+
+pobk_status pobk_plan_get_tiles(pobk_plan_t p, int32_t* ntiles, int32_t* tile_of_row) {
+  if (!p) return fail(POBK_ERR_ARG, "plan is NULL");
+  if (ntiles) *ntiles = p->ntiles;
+  if (tile_of_row) {
+    if (p->tile_of_row.empty()) return fail(POBK_ERR_ARG, "plan has no K2 tiling");
+    std::memcpy(tile_of_row, p->tile_of_row.data(), p->m * sizeof(int32_t));
+  }
+  return POBK_OK;
+}
+
+pobk_status pobk_solve(pobk_plan_t plan, const double* f, double* x, const double* xstar, const pobk_solve_opts* opts,
+                       void* stream, pobk_report* rep) {
+  g_err.clear();
+  pobk_solve_opts o;
+  pobk_status st = check_solve_args(plan, f, x, xstar, o, opts);
+  if (st != POBK_OK) return st;
+  DeviceGuard g(plan->device);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  return solve_device(*plan, f, x, o.stop == POBK_STOP_RSE ? xstar : nullptr, o, (cudaStream_t)stream, rep);
+}
+
+pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const double* xstar, const pobk_solve_opts* opts,
+                            void* stream, pobk_report* rep) {
+  g_err.clear();
+  pobk_solve_opts o;
+  pobk_status st = check_solve_args(plan, f, x, xstar, o, opts);
+  if (st != POBK_OK) return st;
+  DeviceGuard g(plan->device);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  Plan& p = *plan;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = p.m * sizeof(double);
+  if (!p.d_io) CUDA_TRY(dalloc(p, &p.d_io, 3 * p.m));
+  double *df = p.d_io, *dx = p.d_io + p.m, *dxs = p.d_io + 2 * p.m;
+  const bool rse = o.stop == POBK_STOP_RSE;
+  CUDA_TRY(cudaMemcpyAsync(df, f, bytes, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
+  if (rse) CUDA_TRY(cudaMemcpyAsync(dxs, xstar, bytes, cudaMemcpyHostToDevice, s));
+  st = solve_device(p, df, dx, rse ? dxs : nullptr, o, s, rep);
+  if (st != POBK_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return POBK_OK;
+}
+
+pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,
+                             const double* const* xstar, const pobk_solve_opts* opts, void* stream, pobk_report* reps) {
+  g_err.clear();
+  if (nb < 0 || (nb > 0 && (!plans || !f || !x))) return fail(POBK_ERR_ARG, "bad batch arguments");
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = pobk_solve(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
+    if (st != POBK_OK) {
+      g_err = "system " + std::to_string(b) + ": " + g_err;
+      return st;
+    }
+  }
+  return POBK_OK;
+}
+
+pobk_status pobk_residual_sumsq_rows(pobk_plan_t plan, int64_t lo, int64_t hi, const double* f, const double* x, void* stream,
+                                     double* out) {
+  g_err.clear();
+  if (!plan || !f || !x || !out) return fail(POBK_ERR_ARG, "plan, f, x, out must be non-NULL");
+  if (plan->device < 0) return fail(POBK_ERR_NO_DEVICE, "host-only plan");
+  if (lo < 0 || hi > plan->m || lo > hi) return fail(POBK_ERR_ARG, "row range out of bounds");
+  DeviceGuard g(plan->device);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  Plan& p = *plan;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p.d_tmpvec) CUDA_TRY(dalloc(p, &p.d_tmpvec, p.m));
+  if (!p.d_tmpf) CUDA_TRY(dalloc(p, &p.d_tmpf, p.m));
+  long long launches = 0;
+  CUDA_TRY(launch_permute_in(p, f, x, nullptr, p.d_tmpf, p.d_tmpvec, nullptr, s, launches));
+  const bool all = lo == 0 && hi == p.m;
+  CUDA_TRY(residual_sumsq(p, p.d_tmpf, p.d_tmpvec, all ? nullptr : p.A.orig, lo, hi, s, out, launches));
+  return POBK_OK;
+}
+
+pobk_status pobk_residual_norm(pobk_plan_t plan, const double* f, const double* x, void* stream, double* out) {
+  if (!plan) return fail(POBK_ERR_ARG, "plan is NULL");
+  double ss = 0.0;
+  pobk_status st = pobk_residual_sumsq_rows(plan, 0, plan->m, f, x, stream, &ss);
+  if (st == POBK_OK && out) *out = std::sqrt(ss);
+  return st;
+}
+
+void pobk_plan_destroy(pobk_plan_t plan) { destroy_plan(plan); }
+
+}  // extern "C"

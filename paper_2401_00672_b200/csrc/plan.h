@@ -1,0 +1,98 @@
+// The plan: everything pobk_preprocess builds, host and device.  Internal to libpobk.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace pobk {
+
+// Device CSR of A~ in one row order ("storage order"); rows of a schedule step are contiguous
+// for the per-step kernels (K1, K3, K4); K2 keeps its own tile-major copy (k2_plan.h).
+struct DevCSR {
+  int32_t* rp = nullptr;     // [m+1] offsets into col/val (nnz < 2^31)
+  int32_t* col = nullptr;    // [nnz] RCM-frame column ids
+  double* val = nullptr;     // [nnz]
+  double* nrm2 = nullptr;    // [m]   ||a~_i||^2 in storage order
+  int32_t* orig = nullptr;   // [m]   user-frame row of each storage row (perm[rcm row])
+};
+
+struct K2Plan;  // cuda/k2_wavefront.cu
+
+struct Plan {
+  int device = -1;
+  int64_t m = 0, nnz = 0;
+  int32_t nsteps = 0, n_oclass = 0;
+  int64_t bw_before = 0, bw_after = 0;
+  double prep_seconds = 0.0;
+  double thr = 0.0;
+  int kernel = POBK_KERNEL_AUTO;  // family chosen at preprocess
+  int V = 4;                      // lanes per row (fixes the per-row summation tree for every kernel)
+  bool any_overlap = false;
+
+  // host copies (queries, tests)
+  std::vector<int32_t> perm, colour;
+  Schedule sched;
+  std::vector<int32_t> tile_of_row;
+  int32_t ntiles = 0;
+
+  // device
+  int32_t* d_perm = nullptr;      // [m] new -> old
+  DevCSR A;                       // schedule order (step-major)
+  std::vector<int32_t> h_step_ptr;
+  std::vector<uint8_t> h_overlap;
+  double* d_xt = nullptr;         // [m] x~ (RCM frame)
+  double* d_xst = nullptr;        // [m] x~* (RCM frame)
+  double* d_fs = nullptr;         // [m] f~ in storage order
+  double* d_alpha = nullptr;      // [max step size] thr > 0 scratch
+  double* d_partials = nullptr;   // [kMaxReduceBlocks]
+  Ctrl* d_ctrl = nullptr;
+  Ctrl* h_ctrl = nullptr;         // pinned mirror
+  double* d_tmpvec = nullptr;     // [m] residual_norm scratch (x~ of the caller's x)
+  double* d_tmpf = nullptr;       // [m] residual_norm scratch (f in storage order)
+  double* d_io = nullptr;         // [3m] pobk_solve_host staging
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  // K1 device-driven loop
+  cudaGraph_t k1_graph = nullptr;
+  cudaGraphExec_t k1_exec = nullptr;
+  long long k1_nodes_per_sweep = 0;
+
+  K2Plan* k2 = nullptr;
+  size_t k3_smem = 0;
+  int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps
+  uint8_t* k3_overlap = nullptr;   // [nsteps]
+
+  std::vector<void*> allocations;
+};
+
+constexpr int kMaxReduceBlocks = 296;
+
+// cuda/vec_kernels.cu
+// f (user frame) -> fs (storage order); x0, xstar (user frame) -> xt, xst (RCM frame); any input may be NULL
+cudaError_t launch_permute_in(const Plan& p, const double* f, const double* x0, const double* xstar, double* fs,
+                              double* xt, double* xst, cudaStream_t s, long long& launches);
+cudaError_t launch_permute_out(const Plan& p, double* x, cudaStream_t s, long long& launches);
+cudaError_t launch_init_ctrl(const Plan& p, const pobk_solve_opts& o, cudaStream_t s, long long& launches);
+cudaError_t launch_check(const Plan& p, cudaStream_t s);
+cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h);
+cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, const int32_t* orig_lo_hi, int64_t lo,
+                           int64_t hi, cudaStream_t s, double* host_out, long long& launches);
+
+// cuda/k1_launch.cu
+cudaError_t k1_solve(Plan& p, cudaStream_t s, long long& launches);
+// cuda/k3_smem.cu
+bool k3_fits(const Plan& p, size_t& smem_bytes);
+cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches);
+// cuda/k2_wavefront.cu
+bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why);
+cudaError_t k2_solve(Plan& p, cudaStream_t s, long long& launches);
+void k2_free(Plan& p);
+
+}  // namespace pobk
+
+// The opaque ABI handle is the plan itself.
+struct pobk_plan_s : public pobk::Plan {};

@@ -1,0 +1,269 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI, against the oracle on the same
+seeded inputs.
+
+Bars (BASELINE.json north_star): integer work bit-exact; fp64 iterates within
+||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-9 after a fixed sweep count; the same stop sweep +-1.
+thr = 0 iterates are additionally bitwise identical across kernel families and repeat runs."""
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2401_00672_b200 as pk
+    torch.cuda.set_device(0)
+    return pk, torch
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _run(env, s, nsweeps, kernel="auto", thr=0.0, plan=None, pre=None, x0=None):
+    pk, torch = env
+    plan = plan or pk.Plan.from_system(s, kernel=kernel, thr=thr)
+    x = _dev(torch, np.zeros(s.m) if x0 is None else x0)
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), max_sweeps=nsweeps, stop="none")
+    assert rep.sweeps == nsweeps
+    return plan, x.cpu().numpy(), rep
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+SMALL = [("lap2d5_32", None), ("randband_20k", None), ("lap3d7_64", 20), ("geoknn_1m", 30000),
+         ("batch9pt_1024", 100)]
+
+
+@pytest.mark.parametrize("kernel", ["launch", "smem", "wavefront", "auto"])
+@pytest.mark.parametrize("name,n", SMALL)
+def test_fixed_sweeps_parity(env, name, n, kernel):
+    s = gen.make(name, n=n) if n else gen.make(name)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    pk, _ = env
+    try:
+        plan = pk.Plan.from_system(s, kernel=kernel)
+    except pk.PobkError as e:
+        if kernel in ("smem", "wavefront") and e.code == 1:
+            pytest.skip(f"{kernel} not applicable: {e}")
+        raise
+    assert np.array_equal(plan.perm(), pre.perm)
+    nf = 25
+    _, x, rep = _run(env, s, nf, plan=plan)
+    ref = O.run_sweeps(pre, s.f, nf)
+    assert _rel(x, ref) <= REL, (rep.as_dict(), _rel(x, ref))
+
+
+@pytest.mark.parametrize("name,n", [("lap2d5_32", None), ("lap3d7_64", 11), ("randband_20k", 3000),
+                                    ("geoknn_1m", 120000)])
+def test_kernel_families_bitwise_equal(env, name, n):
+    """Same per-row arithmetic contract (common.cuh) -> bitwise-identical iterates (T3)."""
+    pk, _ = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    outs = {}
+    for kernel in ("launch", "smem", "wavefront"):
+        try:
+            _, outs[kernel], _ = _run(env, s, 12, kernel=kernel)
+        except pk.PobkError:
+            continue
+    assert len(outs) >= 2
+    vals = list(outs.values())
+    for v in vals[1:]:
+        assert np.array_equal(v, vals[0]), list(outs)
+
+
+def test_repeatable_bitwise(env):
+    s = gen.make("lap3d7_64", n=24)
+    plan, x1, _ = _run(env, s, 30)
+    _, x2, _ = _run(env, s, 30, plan=plan)
+    assert np.array_equal(x1, x2)
+
+
+def test_stop_sweep_config1_tol_1e6(env):
+    """BASELINE config 1 to the paper's tolerance (RSE < 1e-6): same stop sweep +-1."""
+    pk, torch = env
+    s = gen.make("lap2d5_32")
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, s.x_star, tol=1e-6)
+    assert ref.termination == O.TERM_CONVERGED
+    plan = pk.Plan.from_system(s)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=1e-6)
+    assert rep.termination == 0
+    assert abs(rep.sweeps - ref.sweeps) <= 1, (rep.sweeps, ref.sweeps)
+    assert O.rse(x.cpu().numpy(), s.x_star) < 1e-6
+
+
+@pytest.mark.parametrize("name,n,tol", [("randband_20k", None, 1e-6), ("lap3d7_64", None, 1e-1),
+                                        ("lap2d5_32", None, 1e-3)])
+@pytest.mark.parametrize("kernel", ["auto", "launch"])
+def test_stop_sweep_parity(env, name, n, tol, kernel):
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, s.x_star, tol=tol)
+    plan = pk.Plan.from_system(s, kernel=kernel)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=tol)
+    assert rep.termination == ref.termination
+    assert abs(rep.sweeps - ref.sweeps) <= 1, (rep.sweeps, ref.sweeps)
+    assert abs(rep.final_value - ref.value) <= 1e-9 * ref.value + 1e-15
+
+
+def test_relres_stop_and_residual_norm(env):
+    pk, torch = env
+    s = gen.make("randband_20k")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, stop="relres", tol=1e-8, pre=pre)
+    for kernel in ("launch", "auto"):
+        plan = pk.Plan.from_system(s, kernel=kernel)
+        x = _dev(torch, np.zeros(s.m))
+        f = _dev(torch, s.f)
+        rep = plan.solve(f, x, None, tol=1e-8, stop="relres")
+        assert abs(rep.sweeps - ref.sweeps) <= 1
+        r = plan.residual_norm(f, x)
+        r_ref = O.residual_norm(s.m, s.indptr, s.indices, s.data, s.f, x.cpu().numpy())
+        assert abs(r - r_ref) <= 1e-9 * r_ref
+        # row-sharded residual (C2): shards sum to the whole
+        h = s.m // 3
+        parts = [plan.residual_sumsq_rows(a, b, f, x) for a, b in ((0, h), (h, 2 * h), (2 * h, s.m))]
+        assert abs(np.sqrt(sum(parts)) - r) <= 1e-12 * r
+
+
+@pytest.mark.parametrize("thr", [0.05, 0.12])
+def test_thr_positive_parity(env, thr):
+    """Overlapping categories: simultaneous update with fp64 atomics (a3'), 1e-9 parity."""
+    pk, torch = env
+    s = gen.make("lap2d5_32")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data, thr=thr)
+    assert pre.overlap.any()
+    for kernel in ("launch", "smem"):
+        plan = pk.Plan.from_system(s, thr=thr, kernel=kernel)
+        colour, _, cat_rows = plan.partition()
+        assert np.array_equal(colour, pre.color) and np.array_equal(cat_rows, pre.cat_rows)
+        _, x, _ = _run(env, s, 20, plan=plan)
+        assert _rel(x, O.run_sweeps(pre, s.f, 20)) <= REL
+
+
+@pytest.mark.parametrize("kind", ["hadamard8", "diag"])
+def test_fully_orthogonal_one_sweep(env, kind):
+    pk, torch = env
+    if kind == "diag":
+        import scipy.sparse as sp
+        A = sp.diags(np.linspace(0.5, 2.0, 4000)).tocsr()
+        s = gen.from_csr(kind, A, 4)
+        thr = 0.0
+    else:
+        H = np.array([[1.0]])
+        while H.shape[0] < 8:
+            H = np.block([[H, H], [H, -H]])
+        import scipy.sparse as sp
+        s = gen.from_csr(kind, sp.csr_matrix(H), 5)
+        thr = 0.5
+    plan = pk.Plan.from_system(s, thr=thr)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=1e-12)
+    assert rep.sweeps == 1 and rep.termination == 0
+
+
+def test_edge_cases(env):
+    pk, torch = env
+    import scipy.sparse as sp
+    # m = 1
+    s = gen.from_csr("one", sp.csr_matrix(np.array([[2.0]])), 1)
+    plan = pk.Plan.from_system(s)
+    x = _dev(torch, np.zeros(1))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=1e-12)
+    assert rep.sweeps == 1 and abs(x.item() - s.x_star[0]) < 1e-15
+    # max_sweeps = 0 leaves x0
+    s = gen.make("lap2d5_32")
+    plan = pk.Plan.from_system(s)
+    x0 = np.arange(s.m, dtype=np.float64)
+    x = _dev(torch, x0)
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), max_sweeps=0)
+    assert rep.sweeps == 0 and np.array_equal(x.cpu().numpy(), x0)
+    # all-singleton Nclass (star: every pair of rows overlaps) and a nonzero x0 (resume)
+    star = sp.lil_matrix((60, 60))
+    star[0, :] = 1.0
+    star[:, 0] = 1.0
+    star.setdiag(5.0)
+    s = gen.from_csr("star", star.tocsr(), 2)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    assert pre.n_oclass <= 1
+    x0 = np.random.default_rng(0).standard_normal(s.m)
+    for kernel in ("launch", "smem"):
+        _, x, _ = _run(env, s, 7, kernel=kernel, x0=x0)
+        assert _rel(x, O.run_sweeps(pre, s.f, 7, x0=x0)) <= REL
+    # argument errors: the RSE stop needs x*
+    plan = pk.Plan.from_system(s)
+    with pytest.raises(pk.PobkError):
+        plan.solve(_dev(torch, s.f), _dev(torch, np.zeros(s.m)), None, stop="rse")
+
+
+def test_solve_host_matches_device(env):
+    pk, torch = env
+    s = gen.make("randband_20k")
+    plan = pk.Plan.from_system(s)
+    x = _dev(torch, np.zeros(s.m))
+    r1 = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=1e-6)
+    xh = np.zeros(s.m)
+    r2 = plan.solve_host(s.f.copy(), xh, s.x_star.copy(), tol=1e-6)
+    assert r1.sweeps == r2.sweeps and np.array_equal(xh, x.cpu().numpy())
+
+
+def test_batch_equals_single(env):
+    """T5: a system's iterates are bitwise the same alone or inside a batch."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b, n=48) for b in range(3)]
+    plans = [pk.Plan.from_system(s) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = pk.solve_batch(plans, [_dev(torch, s.f) for s in systems], xs, [_dev(torch, s.x_star) for s in systems],
+                          tol=1e-3)
+    for s, p, xb, r in zip(systems, plans, xs, reps):
+        x = _dev(torch, np.zeros(s.m))
+        r1 = p.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=1e-3)
+        assert r1.sweeps == r.sweeps and np.array_equal(x.cpu().numpy(), xb.cpu().numpy())
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.slow
+def test_config3_full_parity(env):
+    s = gen.make("lap3d7_64")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    plan, x, _ = _run(env, s, 100)
+    assert np.array_equal(plan.perm(), pre.perm)
+    assert np.array_equal(plan.partition()[0], pre.color)
+    assert _rel(x, O.run_sweeps(pre, s.f, 100)) <= REL
+
+
+@pytest.mark.slow
+def test_config4_full_parity(env):
+    """geoknn_1m at full size, in the bench's launch configuration: bit-exact perm/partition and
+    iterates within 1e-9 after N_fix = 100 sweeps."""
+    s = gen.make("geoknn_1m")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    plan, x, rep = _run(env, s, 100)
+    colour, cat_ptr, cat_rows = plan.partition()
+    assert np.array_equal(plan.perm(), pre.perm)
+    assert np.array_equal(colour, pre.color) and np.array_equal(cat_rows, pre.cat_rows)
+    assert np.array_equal(cat_ptr, pre.cat_ptr)
+    assert _rel(x, O.run_sweeps(pre, s.f, 100)) <= REL, rep.as_dict()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("b", [0, 63])
+def test_config5_full_parity(env, b):
+    s = gen.make("batch9pt_1024", b)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    plan, x, _ = _run(env, s, 20)
+    assert np.array_equal(plan.perm(), pre.perm)
+    assert np.array_equal(plan.partition()[0], pre.color)
+    assert _rel(x, O.run_sweeps(pre, s.f, 20)) <= REL
