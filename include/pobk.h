@@ -129,6 +129,20 @@ pobk_status pobk_plan_get_partition(pobk_plan_t plan, int32_t* color, int32_t* c
 /* The K2 tiling (for tests): ntiles, and for each RCM-frame row its tile.  Either may be NULL. */
 pobk_status pobk_plan_get_tiles(pobk_plan_t plan, int32_t* ntiles, int32_t* tile_of_row);
 
+/* Device-layout statistics: kernel family chosen, lanes per row (V), K2 tiles and
+ * chunks, fraction of nonzeros whose x~ column is tile-private (shared memory) and of rows that
+ * touch only private columns, bytes of the K2 chunk stream. */
+typedef struct {
+  int32_t kernel;
+  int32_t lanes;
+  int32_t ntiles;
+  int32_t nchunks;
+  double private_nnz_frac;
+  double interior_row_frac;
+  int64_t stream_bytes;
+} pobk_layout_stats;
+pobk_status pobk_plan_get_layout_stats(pobk_plan_t plan, pobk_layout_stats* out);
+
 /* Iterate from x0 = x_dev (in/out, user frame) until the stop rule; x_dev receives x = P^T x~.
  * f_dev: right-hand side; xstar_dev: exact solution (required for POBK_STOP_RSE, else may be
  * NULL).  Blocks until *rep is filled.  opts NULL = defaults. */

@@ -103,6 +103,11 @@ class Plan:
         L.check(L.lib.pobk_plan_get_tiles(self._h, ctypes.byref(n), L.ptr(t)))
         return n.value, t
 
+    def layout_stats(self) -> dict:
+        st = L.LayoutStats()
+        L.check(L.lib.pobk_plan_get_layout_stats(self._h, ctypes.byref(st)))
+        return st.as_dict()
+
     # ------------------------------------------------------------ solves
     def solve(self, f, x, x_star=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse", check_every: int = 1,
               stream=None) -> Report:

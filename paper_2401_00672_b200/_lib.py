@@ -32,6 +32,17 @@ class SolveOpts(ctypes.Structure):
                 ("check_every", ctypes.c_int32)]
 
 
+class LayoutStats(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("lanes", ctypes.c_int32), ("ntiles", ctypes.c_int32),
+                ("nchunks", ctypes.c_int32), ("private_nnz_frac", ctypes.c_double),
+                ("interior_row_frac", ctypes.c_double), ("stream_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["kernel"] = KERNEL_NAME.get(self.kernel, self.kernel)
+        return d
+
+
 class Report(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int64), ("termination", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("final_value", ctypes.c_double), ("solve_seconds", ctypes.c_double),
@@ -62,6 +73,7 @@ SIGNATURES = {
     "pobk_plan_get_perm": (I32, [P, P]),
     "pobk_plan_get_partition": (I32, [P, P, P, P]),
     "pobk_plan_get_tiles": (I32, [P, ctypes.POINTER(I32), P]),
+    "pobk_plan_get_layout_stats": (I32, [P, ctypes.POINTER(LayoutStats)]),
     "pobk_solve": (I32, [P, P, P, P, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report)]),
     "pobk_solve_host": (I32, [P, P, P, P, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report)]),
     "pobk_solve_batch": (I32, [ctypes.POINTER(P), I32, P, P, P, ctypes.POINTER(SolveOpts), P, P]),
@@ -75,7 +87,7 @@ SIGNATURES = {
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2401_00672_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2401_00672_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():

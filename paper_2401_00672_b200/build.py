@@ -1,6 +1,6 @@
 """Build libpobk.so in-tree (nvcc for sm_100a; host code with -ffp-contract=off).
 
-    python -m paper_2401_00672_b200.build [--force]
+    python paper_2401_00672_b200/build.py [--force]   (by path: importing the package loads the library)
 """
 from __future__ import annotations
 

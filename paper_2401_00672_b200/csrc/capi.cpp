@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -57,12 +58,22 @@ cudaError_t upload(Plan& p, T** ptr, const T* src, size_t count) {
   return e;
 }
 
-// Lanes per row: nearest power of two to half the mean row length, in [2, 32]; fixes the
-// per-row summation tree shared by all kernel families (common.cuh).
-int choose_lanes(int64_t m, int64_t nnz) {
-  const double half = 0.5 * (double)nnz / (double)m;
-  int v = 2;
-  while (v < 32 && (double)(2 * v) <= half * 1.5) v *= 2;
+// Lanes per row V: the smallest power of two such that 4 lanes' worth of entries
+// (4V) covers the 99.5th-percentile row length, so almost every lane holds its <= 4 entries in
+// registers between the gather and the scatter (no serial reloads).  V fixes the per-row summation
+// tree shared by all kernel families (common.cuh).
+int choose_lanes(const HostCSR& A) {
+  if (const char* env = std::getenv("POBK_LANES")) {  // development override (must be a power of two)
+    const int v = std::atoi(env);
+    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) return v;
+  }
+  std::vector<int64_t> len(A.m);
+  for (int64_t i = 0; i < A.m; i++) len[i] = A.ptr[i + 1] - A.ptr[i];
+  const int64_t k = std::min<int64_t>(A.m - 1, (int64_t)(0.995 * (double)(A.m - 1)));
+  std::nth_element(len.begin(), len.begin() + k, len.end());
+  const int64_t p995 = len[k];
+  int v = 1;
+  while (v < 32 && 4 * v < p995) v *= 2;
   return v;
 }
 
@@ -147,10 +158,14 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
   CUDA_TRY(launch_permute_in(p, f, x, xstar, p.d_fs, p.d_xt, o.stop == POBK_STOP_RSE ? p.d_xst : nullptr, s, launches));
   CUDA_TRY(launch_init_ctrl(p, o, s, launches));
   CUDA_TRY(cudaEventRecord(p.ev[1], s));
+  // K2 evaluates RSE and fixed counts in-kernel; a RELRES stop runs on the K1 graph loop (its
+  // check kernel carries the fused residual SpMV + norm).
+  int used = p.kernel;
+  if (used == POBK_KERNEL_WAVEFRONT && o.stop == POBK_STOP_RELRES) used = POBK_KERNEL_LAUNCH;
   if (o.max_sweeps > 0) {
-    switch (p.kernel) {
+    switch (used) {
       case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
-      case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, s, launches)); break;
+      case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, f, s, launches)); break;
       default: CUDA_TRY(k1_solve(p, s, launches)); break;
     }
   }
@@ -163,11 +178,11 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
   CUDA_TRY(cudaEventElapsedTime(&t_all, p.ev[0], p.ev[3]));
   CUDA_TRY(cudaEventElapsedTime(&t_sw, p.ev[1], p.ev[2]));
   const Ctrl& c = *p.h_ctrl;
-  if (p.kernel == POBK_KERNEL_LAUNCH && o.max_sweeps > 0) launches += c.sweeps * p.k1_nodes_per_sweep;
+  if (used == POBK_KERNEL_LAUNCH && o.max_sweeps > 0) launches += c.sweeps * p.k1_nodes_per_sweep;
   if (rep) {
     rep->sweeps = o.max_sweeps > 0 ? c.sweeps : 0;
     rep->termination = c.term;
-    rep->kernel = p.kernel;
+    rep->kernel = used;
     rep->final_value = (o.stop == POBK_STOP_NONE) ? NAN : c.value;
     rep->solve_seconds = t_all * 1e-3;
     rep->sweep_seconds = t_sw * 1e-3;
@@ -265,7 +280,7 @@ pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* co
         return fail(POBK_ERR_UNSTABLE_THR, why);
       }
     }
-    p->V = choose_lanes(m, p->nnz);
+    p->V = choose_lanes(At);
     if (device >= 0) {
       pobk_status st = build_device(*p, At, nrm2, o.tile_rows);
       if (st != POBK_OK) {
@@ -320,6 +335,22 @@ pobk_status pobk_plan_get_tiles(pobk_plan_t p, int32_t* ntiles, int32_t* tile_of
   if (tile_of_row) {
     if (p->tile_of_row.empty()) return fail(POBK_ERR_ARG, "plan has no K2 tiling");
     std::memcpy(tile_of_row, p->tile_of_row.data(), p->m * sizeof(int32_t));
+  }
+  return POBK_OK;
+}
+
+pobk_status pobk_plan_get_layout_stats(pobk_plan_t p, pobk_layout_stats* out) {
+  if (!p || !out) return fail(POBK_ERR_ARG, "plan and out must be non-NULL");
+  std::memset(out, 0, sizeof(*out));
+  out->kernel = p->kernel;
+  out->lanes = p->V;
+  K2Stats st;
+  if (k2_stats(*p, st)) {
+    out->ntiles = st.T;
+    out->nchunks = st.nchunks;
+    out->private_nnz_frac = st.private_frac;
+    out->interior_row_frac = st.interior_frac;
+    out->stream_bytes = st.stream_bytes;
   }
   return POBK_OK;
 }

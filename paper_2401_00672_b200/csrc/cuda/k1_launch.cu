@@ -104,6 +104,7 @@ cudaError_t build_graph(Plan& p) {
     return e;
   long long nodes = 0;
   switch (p.V) {
+    case 1: e = capture_sweep<1>(p, cs, nodes); break;
     case 2: e = capture_sweep<2>(p, cs, nodes); break;
     case 4: e = capture_sweep<4>(p, cs, nodes); break;
     case 8: e = capture_sweep<8>(p, cs, nodes); break;

@@ -185,6 +185,7 @@ bool k3_fits(const Plan& p, size_t& bytes) {
 cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches) {
   launches++;
   switch (p.V) {
+    case 1: return launch<1>(p, s);
     case 2: return launch<2>(p, s);
     case 4: return launch<4>(p, s);
     case 8: return launch<8>(p, s);

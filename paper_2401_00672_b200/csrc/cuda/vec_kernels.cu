@@ -222,6 +222,7 @@ static cudaError_t launch_check_v(const Plan& p, cudaStream_t s, cudaGraphCondit
 
 cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h) {
   switch (p.V) {
+    case 1: return launch_check_v<1>(p, s, h, 1);
     case 2: return launch_check_v<2>(p, s, h, 1);
     case 4: return launch_check_v<4>(p, s, h, 1);
     case 8: return launch_check_v<8>(p, s, h, 1);
@@ -232,6 +233,7 @@ cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphCondition
 
 cudaError_t launch_check(const Plan& p, cudaStream_t s) {
   switch (p.V) {
+    case 1: return launch_check_v<1>(p, s, 0, 0);
     case 2: return launch_check_v<2>(p, s, 0, 0);
     case 4: return launch_check_v<4>(p, s, 0, 0);
     case 8: return launch_check_v<8>(p, s, 0, 0);
@@ -250,6 +252,7 @@ cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, co
   if (e != cudaSuccess) return e;
   const int B = reduce_blocks(p.m);
   switch (p.V) {
+    case 1: k_resid<1><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
     case 2: k_resid<2><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
     case 4: k_resid<4><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
     case 8: k_resid<8><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;

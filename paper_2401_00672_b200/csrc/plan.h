@@ -89,7 +89,9 @@ bool k3_fits(const Plan& p, size_t& smem_bytes);
 cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches);
 // cuda/k2_wavefront.cu
 bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why);
-cudaError_t k2_solve(Plan& p, cudaStream_t s, long long& launches);
+cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
+struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; };
+bool k2_stats(const Plan& p, K2Stats& st);
 void k2_free(Plan& p);
 
 }  // namespace pobk
