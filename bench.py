@@ -300,7 +300,7 @@ def main():
         "config": {"workload": s0.name if a.config != "batch9pt_1024" else f"{a.config} x8 per GPU",
                    "m": s0.m, "nnz": s0.nnz, "systems_per_gpu": len(systems), "tol_rse": tol, "stop": "rse",
                    "sweeps_per_solve": all_reps[0].sweeps, "kernel": all_reps[0].as_dict()["kernel"],
-                   "lanes": stats["lanes"], "tiles": stats["ntiles"], "private_nnz_frac": round(stats["private_nnz_frac"], 4),
+                   "tiles": stats["ntiles"], "private_nnz_frac": round(stats["private_nnz_frac"], 4),
                    "nsteps": plans[0].nsteps, "bandwidth_rcm": plans[0].bw_after,
                    "preprocess_s": round(plans[0].preprocess_seconds, 3),
                    "l2": "inputs larger than L2 (A stream %.0f MB > 126 MB), no flush" % (B / 1e6),

@@ -129,14 +129,14 @@ pobk_status pobk_plan_get_partition(pobk_plan_t plan, int32_t* color, int32_t* c
 /* The K2 tiling (for tests): ntiles, and for each RCM-frame row its tile.  Either may be NULL. */
 pobk_status pobk_plan_get_tiles(pobk_plan_t plan, int32_t* ntiles, int32_t* tile_of_row);
 
-/* Device-layout statistics: kernel family chosen, lanes per row (V), K2 tiles and
- * chunks, fraction of nonzeros whose x~ column is tile-private (shared memory) and of rows that
- * touch only private columns, bytes of the K2 chunk stream. */
+/* Device-layout statistics: kernel family chosen, K2 tiles and chunks, fraction
+ * of nonzeros whose x~ column is tile-private (shared memory) and of rows that touch only private
+ * columns, bytes of the K2 chunk stream. */
 typedef struct {
   int32_t kernel;
-  int32_t lanes;
   int32_t ntiles;
   int32_t nchunks;
+  int32_t reserved;
   double private_nnz_frac;
   double interior_row_frac;
   int64_t stream_bytes;

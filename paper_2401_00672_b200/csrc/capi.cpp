@@ -58,25 +58,6 @@ cudaError_t upload(Plan& p, T** ptr, const T* src, size_t count) {
   return e;
 }
 
-// Lanes per row V: the smallest power of two such that 4 lanes' worth of entries
-// (4V) covers the 99.5th-percentile row length, so almost every lane holds its <= 4 entries in
-// registers between the gather and the scatter (no serial reloads).  V fixes the per-row summation
-// tree shared by all kernel families (common.cuh).
-int choose_lanes(const HostCSR& A) {
-  if (const char* env = std::getenv("POBK_LANES")) {  // development override (must be a power of two)
-    const int v = std::atoi(env);
-    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) return v;
-  }
-  std::vector<int64_t> len(A.m);
-  for (int64_t i = 0; i < A.m; i++) len[i] = A.ptr[i + 1] - A.ptr[i];
-  const int64_t k = std::min<int64_t>(A.m - 1, (int64_t)(0.995 * (double)(A.m - 1)));
-  std::nth_element(len.begin(), len.begin() + k, len.end());
-  const int64_t p995 = len[k];
-  int v = 1;
-  while (v < 32 && 4 * v < p995) v *= 2;
-  return v;
-}
-
 void destroy_plan(Plan* p) {
   if (!p) return;
   if (p->device >= 0) {
@@ -280,7 +261,6 @@ pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* co
         return fail(POBK_ERR_UNSTABLE_THR, why);
       }
     }
-    p->V = choose_lanes(At);
     if (device >= 0) {
       pobk_status st = build_device(*p, At, nrm2, o.tile_rows);
       if (st != POBK_OK) {
@@ -343,7 +323,6 @@ pobk_status pobk_plan_get_layout_stats(pobk_plan_t p, pobk_layout_stats* out) {
   if (!p || !out) return fail(POBK_ERR_ARG, "plan and out must be non-NULL");
   std::memset(out, 0, sizeof(*out));
   out->kernel = p->kernel;
-  out->lanes = p->V;
   K2Stats st;
   if (k2_stats(*p, st)) {
     out->ntiles = st.T;

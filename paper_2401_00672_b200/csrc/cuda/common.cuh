@@ -1,25 +1,20 @@
 // Device helpers shared by the sweep kernels (K1, K2, K3) and the check kernels.
 //
-// THE PER-ROW ARITHMETIC CONTRACT.  Every sweep kernel computes a row's
-// projection (Eq 1.2) with exactly these operations, so all kernel families
-// produce bitwise-identical iterates for thr = 0:
-//   lane l (0 <= l < V) of the row's V-lane vector:  acc_l = 0; for p = p0+l, p0+l+V, ... < p1:
-//                                                     acc_l = fma(a_p, x_{col p}, acc_l)
-//   xor-butterfly over the V lanes (offsets V/2, ..., 1): acc += shfl_xor(acc, o)
-//   alpha = (f_i - acc) / nrm2_i                       (division, as in Eq 1.2)
-//   x_{col p} = fma(alpha, a_p, x_{col p})            (for the lane's own entries)
+// THE PER-ROW ARITHMETIC CONTRACT.  Every sweep kernel applies a row's
+// projection (Eq 1.2) with exactly the operations of the oracle's O7, each
+// rounded separately (no FMA contraction):
+//     s = 0;  for p ascending:  s = s + (a_p * x_{col p})       (dmul_rn, then dadd_rn)
+//     alpha = (f_i - s) / nrm2_i                                   (dsub_rn, ddiv_rn)
+//     for p:  x_{col p} = x_{col p} + (alpha * a_p)                (dmul_rn, then dadd_rn)
+// Because the rows of one category have disjoint supports (thr = 0), the order in which a
+// category's rows are applied cannot change any value, so every kernel family reproduces the
+// oracle's iterates BIT FOR BIT, whatever its parallel schedule.  (thr > 0 overlapping categories
+// use fp64 atomics for the scatter: order-dependent, parity to 1e-9.)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace pobk {
-
-template <int V>
-__device__ __forceinline__ double vec_sum(double v) {
-#pragma unroll
-  for (int o = V / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, V);
-  return v;
-}
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ void st_cg(double* p, double v) { __stcg(p, v); }
@@ -36,6 +31,28 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// One row of Eq 1.2 by one thread, x in any memory space reachable through a generic pointer.
+// Returns alpha.
+__device__ __forceinline__ double row_project(const int32_t* __restrict__ col, const double* __restrict__ val,
+                                              int p0, int p1, double f, double nrm2, double* x) {
+  double s = 0.0;
+  for (int p = p0; p < p1; p++) s = __dadd_rn(s, __dmul_rn(val[p], x[col[p]]));
+  const double alpha = __ddiv_rn(__dsub_rn(f, s), nrm2);
+  for (int p = p0; p < p1; p++) {
+    const int c = col[p];
+    x[c] = __dadd_rn(x[c], __dmul_rn(alpha, val[p]));
+  }
+  return alpha;
+}
+
+// Eq 1.2 residual part only (thr > 0 pass 1, RELRES): alpha of a row at the current x.
+__device__ __forceinline__ double row_dot(const int32_t* __restrict__ col, const double* __restrict__ val, int p0,
+                                          int p1, const double* x) {
+  double s = 0.0;
+  for (int p = p0; p < p1; p++) s = __dadd_rn(s, __dmul_rn(val[p], x[col[p]]));
+  return s;
 }
 
 // Deterministic block sum (fixed tree): every thread passes its value; thread 0 gets the sum.

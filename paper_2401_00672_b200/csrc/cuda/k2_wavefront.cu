@@ -1,25 +1,28 @@
-// K2: persistent tiled wavefront sweep.
+// K2: persistent tiled wavefront sweep, warp-specialised.
 //
 // The rows of A~ are split into T tiles (one CTA per SM, cooperative launch).  A schedule step
-// (a category of pairwise-orthogonal rows) restricted to one tile is a "task".
-// Sequential semantics of the sweep (Alg 5 loop) only constrain rows that share
-// a column, so a tile's task k may run as soon as every NEIGHBOUR tile (one sharing a column with
-// it) has finished its tasks < k: per-tile progress counters (release/acquire at gpu scope)
-// replace the grid-wide barrier between categories.  Results are bitwise those of K1/K3 (same
-// per-row contract, common.cuh).
+// (a category of pairwise-orthogonal rows) restricted to one tile is a "task".  The
+// sequential semantics of a sweep (Alg 5 loop) only order rows that share a
+// column, so a tile's task k may run once every NEIGHBOUR tile (one sharing a column with it) has
+// finished its tasks < k: per-tile progress counters at gpu scope replace the grid-wide barrier
+// between categories.  Results are bitwise those of K1/K3 (same per-row contract, common.cuh).
 //
-//   x~ columns touched by one tile only ("private") live in that CTA's shared memory for the
-//   whole solve; the rest ("shared") live in global memory and are accessed at L2 (ld/st .cg).
-//   Within a task, rows touching only private columns ("interior") run before the neighbour wait;
-//   rows touching a shared column ("boundary") run after it.
-//
-//   The tile's matrix data (val, col, row extents, f~, ||a~_i||^2) is a sequence of <= 28 KB chunks
-//   streamed by 1-D TMA (cp.async.bulk) into a 4-slot shared-memory ring, S-1 chunks ahead of the
-//   consumer and across task and sweep boundaries (A does not depend on x~).
-//
-//   The RSE is accumulated by the LAST writer of every column in the sweep (the row
-//   of highest step touching it), so no extra pass over x~ is needed; a grid-wide last-arriver
-//   reduction in tile order decides the stop once per checked sweep.
+//  * x~ columns touched by one tile only ("private") live in that CTA's shared memory for the
+//    whole solve; the rest ("shared") live in global memory and are accessed at L2 (ld/st .cg).
+//    Within a task, rows touching only private columns ("interior") run before the neighbour
+//    wait; rows touching a shared column ("boundary") run after it.
+//  * The tile's matrix data (val, col, row extents, f~, ||a~_i||^2) is a sequence of <= 40 KB
+//    chunks streamed by 1-D TMA (cp.async.bulk, L2 evict-first) into a 3-slot shared-memory ring,
+//    across task and sweep boundaries (A does not depend on x~).
+//  * Warp 31 is the CONTROL warp: it issues the TMA copies as slots free up, polls the neighbours'
+//    progress for the next boundary task and releases it to the compute warps, publishes the
+//    tile's progress when all compute warps finished a task (gpu-scope fence off the compute
+//    critical path), and runs the per-sweep stop decision.  Warps 0..30 COMPUTE: they flow
+//    through the chunks without CTA-wide barriers; one named barrier per task orders
+//    consecutive tasks inside the tile.
+//  * The RSE is accumulated by the LAST writer of every column in the sweep (the
+//    row of highest step touching it): no extra pass over x~; per-warp partials are reduced in a
+//    fixed order, tiles in tile order (deterministic).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,12 +40,14 @@
 namespace pobk {
 
 namespace {
-constexpr int kNT = 1024;          // threads per CTA
-constexpr int kSlots = 3;          // TMA ring depth
+constexpr int kNT = 1024;           // threads per CTA
+constexpr int kNCW = 31;            // compute warps (warp 31 = control)
+constexpr int kSlots = 3;           // TMA ring depth
 constexpr int kChunkCap = 40 * 1024;
-constexpr int kNbMax = 16;         // max neighbour tiles
-constexpr int kMaxChunks = 1024;   // max chunks per tile (chunk metadata lives in shared memory)
-constexpr int kFlagStride = 32;    // ints between progress counters (one 128-B line each)
+constexpr int kEPT = 4;             // entries per compute thread per chunk (chunk nnz <= kEPT * 992)
+constexpr int kNbMax = 16;          // max neighbour tiles
+constexpr int kMaxChunks = 1024;    // max chunks per tile (metadata lives in shared memory)
+constexpr int kFlagStride = 32;     // ints between progress counters (one 128-B line each)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr unsigned kShared = 0x80000000u, kLast = 0x40000000u, kIdx = 0x3FFFFFFFu;
 constexpr int kFirstBoundary = 1, kLastOfTask = 2;
@@ -63,16 +68,18 @@ struct ChunkLayout {
 };
 
 struct ChunkMeta {
-  int rows, nnz, step, flags;
-  int k_next;   // last chunk of a task: the tile's next task step (>= nsteps: next sweep)
-  int pad0, pad1, pad2;
-  long long off;  // byte offset of the block in the stream
+  int rows, nnz, task, flags;  // task = index in the tile's per-sweep task list
+  long long off;               // byte offset of the block in the stream
+};
+
+struct TaskMeta {
+  int step, k_next, boundary, pad;  // k_next >= nsteps: first task of the next sweep
 };
 
 struct SyncState {
   unsigned int arrive[2];
   int pad0[30];
-  int epoch;      // = sweeps decided
+  int epoch;  // = sweeps decided
   int stop;
   int pad1[30];
 };
@@ -81,21 +88,33 @@ struct K2Args {
   const unsigned char* stream;
   const long long* tile_off;  // [T] byte offset of each tile's first chunk
   const ChunkMeta* meta;
-  const int* tile_chunk;  // [T+1]
-  const int* nbr;         // [T*kNbMax], -1 padded
-  const int* pmap_ptr;    // [T+1]
-  const int* pmap;        // private columns (global ids), tile by tile
-  const int* k_first;     // [T]
-  double* xg;             // x~ (RCM frame); authoritative for shared columns
-  const double* xst;      // x~*
-  int* progress;          // [T*kFlagStride]
+  const int* tile_chunk;      // [T+1]
+  const TaskMeta* tmeta;
+  const int* tile_task;       // [T+1]
+  const int* nbr;             // [T*kNbMax], -1 padded
+  const int* pmap_ptr;        // [T+1]
+  const int* pmap;            // private columns (global ids), tile by tile
+  double* xg;                 // x~ (RCM frame); authoritative for shared columns
+  const double* xst;          // x~*
+  int* progress;              // [T*kFlagStride]
   SyncState* sync;
-  double* partials;       // [2*T]
+  double* partials;           // [2*T]
   Ctrl* ctrl;
   int nsteps, T;
-  int nck_max, np_max;  // shared-memory sizing
-  unsigned long long* prof;  // optional [T*8] phase clocks (POBK_K2_PROFILE=1), else NULL
-  int debug;                 // development-only timing experiments (POBK_K2_DEBUG): 1 relaxed publish, 2 no wait
+  int nck_max, ntask_max, np_max;  // shared-memory sizing
+  int debug;                       // development timing experiments (POBK_K2_DEBUG): 2 = no neighbour wait
+  unsigned long long* prof;        // optional [T*8] compute-warp phase clocks (POBK_K2_PROFILE=1)
+};
+
+// shared-memory control block
+struct Ctl {
+  unsigned long long full[4];  // TMA completion mbarriers
+  int released[4];             // compute-warp releases per slot (cumulative)
+  int go;                      // task sequence numbers released to the compute warps
+  int done;                    // compute-warp task completions (cumulative)
+  int epoch;                   // sweeps decided
+  int stop;
+  double part[32];             // per-compute-warp RSE partials
 };
 
 // ------------------------------------------------------------------ PTX helpers (TMA, mbarrier)
@@ -128,37 +147,48 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ int ld_vol_shared(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
-template <int V>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;                                             // kSlots * kChunkCap
-  unsigned long long* mbar = (unsigned long long*)(smem + kSlots * kChunkCap);
-  double* red = (double*)(mbar + 4);                                      // 32 doubles (mbar area padded to 32 B)
-  int4* cmeta = (int4*)(red + 32);                                        // [nck_max] {rows, nnz, step<<2|flags, k_next}
-  int* coff = (int*)(cmeta + a.nck_max);                                  // [nck_max] byte offset from the tile base
-  double* xloc = (double*)(coff + ((a.nck_max + 3) & ~3));                // [np_max] private x~
-  double* xsloc = xloc + a.np_max;                                        // [np_max] private x~* (RSE stop)
-  __shared__ int s_stop;
+  unsigned char* ring = smem;                                   // kSlots * kChunkCap
+  Ctl* ctl = (Ctl*)(smem + kSlots * kChunkCap);
+  int4* cmeta = (int4*)(ctl + 1);                               // [nck_max] {rows, nnz, task, flags}
+  int* coff = (int*)(cmeta + a.nck_max);                        // [nck_max] byte offset from the tile base
+  int4* tmeta = (int4*)(coff + ((a.nck_max + 3) & ~3));          // [ntask_max]
+  double* xloc = (double*)(tmeta + a.ntask_max);                // [np_max] private x~
+  double* xsloc = xloc + a.np_max;                              // [np_max] private x~* (RSE stop)
 
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, wl = tid & 31;
   const int c0 = a.tile_chunk[t], nck = a.tile_chunk[t + 1] - c0;
+  const int j0 = a.tile_task[t], ntask = a.tile_task[t + 1] - j0;
   const int q0 = a.pmap_ptr[t], np = a.pmap_ptr[t + 1] - q0;
   const int nsteps = a.nsteps;
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
-  const double tol = a.ctrl->tol, den = a.ctrl->den;
-  const unsigned char* tbase = a.stream + a.tile_off[t];
 
   if (tid == 0) {
-    for (int i = 0; i < kSlots; i++) mbar_init(mbar + i, 1);
+    for (int i = 0; i < 4; i++) {
+      mbar_init(&ctl->full[i], 1);
+      ctl->released[i] = 0;
+    }
+    ctl->go = 0;
+    ctl->done = 0;
+    ctl->epoch = 0;
+    ctl->stop = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_stop = 0;
   }
   for (int j = tid; j < nck; j += kNT) {
     const ChunkMeta mt = a.meta[c0 + j];
-    cmeta[j] = make_int4(mt.rows, mt.nnz, (mt.step << 2) | mt.flags, mt.k_next);
+    cmeta[j] = make_int4(mt.rows, mt.nnz, mt.task, mt.flags);
     coff[j] = (int)(mt.off - a.tile_off[t]);
+  }
+  for (int j = tid; j < ntask; j += kNT) {
+    const TaskMeta tm = a.tmeta[j0 + j];
+    tmeta[j] = make_int4(tm.step, tm.k_next, tm.boundary, 0);
   }
   for (int j = tid; j < np; j += kNT) {
     const int gcol = a.pmap[q0 + j];
@@ -167,116 +197,214 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   }
   __syncthreads();
 
-  const unsigned long long pol = policy_evict_first();
-  auto issue = [&](long long g) {  // thread 0 only
-    const int slot = (int)(g % kSlots);
-    const int c = (int)(g % nck);
-    const int4 mt = cmeta[c];
-    const int bytes = ChunkLayout(mt.x, mt.y).bytes;
-    mbar_expect_tx(mbar + slot, bytes);
-    tma_load_1d(ring + slot * kChunkCap, tbase + coff[c], bytes, mbar + slot, pol);
-  };
-  long long issued = 0;
-  if (tid == 0 && nck > 0)
-    for (; issued < kSlots - 1; issued++) issue(issued);
-
-  const int lane = tid % V, vec = tid / V, nvec = kNT / V;
-  const int warp = tid >> 5, wl = tid & 31;
-  int my_nb = -1;  // warp 0: lane j polls neighbour j
-  if (warp == 0 && wl < kNbMax) my_nb = a.nbr[t * kNbMax + wl];
-  double acc_rse = 0.0;
-  long long sweep = 0, g = 0;
-  unsigned long long pr[6] = {0, 0, 0, 0, 0, 0};  // nbwait, mbarwait, compute, publish, barrier, total
-  const unsigned long long t_start = clock64();
-  while (true) {
-    acc_rse = 0.0;  // only the checked sweep's last-writer events count
-    for (int i = 0; i < nck; i++, g++) {
-      if (tid == 0) {
-        issue(issued);
-        issued++;
-      }
-      const int4 mt = cmeta[i];
-      const int rows = mt.x, nnz = mt.y, step = mt.z >> 2, flags = mt.z & 3;
-      unsigned long long c_a = clock64();
-      if ((flags & kFirstBoundary) && !(a.debug & 2)) {
-        if (warp == 0) {
-          const int need = (int)(sweep * nsteps + step);
-          if (my_nb >= 0) {
-            const int* pf = a.progress + my_nb * kFlagStride;
-            while (ld_acquire(pf) < need) {
-            }
+  if (warp == kNCW) {
+    // ================================================================ control warp
+    const unsigned long long pol = policy_evict_first();
+    const int my_nb = wl < kNbMax ? a.nbr[t * kNbMax + wl] : -1;
+    const unsigned char* tbase = a.stream + a.tile_off[t];
+    long long g_issue = 0;   // next chunk sequence to issue
+    long long j_go = 0;      // next task sequence to release
+    long long j_pub = 0;     // next task sequence to publish
+    long long sweep = 0;     // sweeps completed (decided)
+    bool finished = (maxs <= 0);
+    while (!finished) {
+      // (1) TMA: keep the ring full (a slot is free once all compute warps released its last use);
+      //     never more than one sweep ahead of the decided sweep
+      if (nck > 0) {
+        while (g_issue < (sweep + 2) * (long long)nck) {
+          const int slot = (int)(g_issue % kSlots);
+          const long long use = g_issue / kSlots;
+          if (use > 0 && ld_vol_shared(&ctl->released[slot]) < (int)(use * kNCW)) break;
+          if (wl == 0) {
+            const int c = (int)(g_issue % nck);
+            const int4 mt = cmeta[c];
+            const int bytes = ChunkLayout(mt.x, mt.y).bytes;
+            mbar_expect_tx(&ctl->full[slot], bytes);
+            tma_load_1d(ring + slot * kChunkCap, tbase + coff[c], bytes, &ctl->full[slot], pol);
           }
           __syncwarp();
+          g_issue++;
         }
-        __syncthreads();
       }
-      const int slot = (int)(g % kSlots);
-      unsigned long long c_b = clock64();
-      mbar_wait(mbar + slot, (unsigned)((g / kSlots) & 1));
-      unsigned long long c_c = clock64();
-      const unsigned char* blk = ring + slot * kChunkCap;
-      const ChunkLayout L(rows, nnz);
-      const double* val = (const double*)(blk + L.o_val);
-      const double* fv = (const double*)(blk + L.o_f);
-      const double* nv = (const double*)(blk + L.o_n);
-      const unsigned* col = (const unsigned*)(blk + L.o_col);
-      const int* rp = (const int*)(blk + L.o_rp);
-      for (int base = 0; base < rows; base += nvec) {
-        const int r = base + vec;
-        const bool act = r < rows;
-        const int p0 = act ? rp[r] : 0, p1 = act ? rp[r + 1] : 0;
-        constexpr int KC = 4;
-        unsigned cc[KC];
-        double av[KC], xv[KC], sv[KC];
+      // (2) release the next task of this sweep once its neighbours are far enough
+      if (ntask > 0 && j_go < (sweep + 1) * (long long)ntask) {
+        const int4 tm = tmeta[(int)(j_go % ntask)];
+        const long long sw = j_go / ntask;
+        bool ok = true;
+        if (tm.z && !(a.debug & 2)) {
+          const int need = (int)(sw * nsteps + tm.x);
+          const int v = my_nb >= 0 ? ld_relaxed(a.progress + my_nb * kFlagStride) : need;
+          ok = __all_sync(0xffffffffu, v >= need);
+        }
+        if (ok) {
+          if (tm.z) __threadfence();  // acquire the neighbours' writes at gpu scope ...
+          j_go++;
+          if (wl == 0) *(volatile int*)&ctl->go = (int)j_go;  // ... and hand them to the CTA
+          __syncwarp();
+        }
+      }
+      // (3) publish finished tasks (all compute warps reported the task)
+      if (ntask > 0 && j_pub < j_go && ld_vol_shared(&ctl->done) >= (int)((j_pub + 1) * kNCW)) {
+        const int4 tm = tmeta[(int)(j_pub % ntask)];
+        const long long sw = j_pub / ntask;
+        __threadfence();
+        if (wl == 0)
+          asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(a.progress + t * kFlagStride),
+                       "r"((int)(sw * nsteps + tm.y))
+                       : "memory");
+        __syncwarp();
+        j_pub++;
+      }
+      // (4) end of sweep: every task of the sweep published (or no tasks)
+      if ((ntask == 0) || (j_pub >= (sweep + 1) * (long long)ntask)) {
+        const long long s1 = sweep + 1;
+        const bool due = mode != POBK_STOP_NONE && ((s1 % every) == 0 || s1 >= maxs);
+        int stop = 0;
+        if (due) {
+          if (wl == 0) {
+            double part = 0.0;
+            if (ntask > 0)
+              for (int w = 0; w < kNCW; w++) part += ((volatile double*)ctl->part)[w];
+            const int par = (int)(s1 & 1);
+            a.partials[par * a.T + t] = part;
+            __threadfence();
+            const unsigned old = atomicAdd(&a.sync->arrive[par], 1u);
+            if (old == (unsigned)a.T - 1) {
+              __threadfence();
+              double tot = 0.0;
+              for (int b = 0; b < a.T; b++) tot += ld_cg(a.partials + par * a.T + b);
+              const double v = sqrt(tot) / sqrt(a.ctrl->den);
+              int st = 0, term = POBK_TERM_MAX_SWEEPS;
+              if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
+              else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
+              else if (s1 >= maxs) st = 1;
+              a.sync->arrive[par] = 0;
+              a.sync->stop = st;
+              a.ctrl->value = v;
+              a.ctrl->sweeps = s1;
+              a.ctrl->term = term;
+              __threadfence();
+              st_release(&a.sync->epoch, (int)s1);
+            } else {
+              while (ld_relaxed(&a.sync->epoch) < (int)s1) {
+              }
+              __threadfence();
+            }
+            stop = ld_relaxed(&a.sync->stop);
+          }
+          stop = __shfl_sync(0xffffffffu, stop, 0);
+        } else if (s1 >= maxs) {
+          stop = 1;
+          if (t == 0 && wl == 0) {
+            a.ctrl->sweeps = s1;
+            a.ctrl->term = POBK_TERM_MAX_SWEEPS;
+          }
+        }
+        sweep = s1;
+        if (wl == 0) {
+          *(volatile int*)&ctl->stop = stop;
+          __threadfence_block();
+          *(volatile int*)&ctl->epoch = (int)sweep;
+        }
+        __syncwarp();
+        if (stop) finished = true;
+      }
+    }
+    // drain the TMA copies issued beyond the consumed ones
+    if (wl == 0 && nck > 0) {
+      const long long consumed = sweep * nck;
+      for (long long h = consumed; h < g_issue; h++)
+        mbar_wait(&ctl->full[(int)(h % kSlots)], (unsigned)((h / kSlots) & 1));
+    }
+  } else {
+    // ================================================================ compute warps
+    // Entry-parallel, three phases per chunk (the oracle's arithmetic, common.cuh):
+    //   A  every thread takes entries p = cid + e*NC: gathers x~ (smem or L2) and forms
+    //      a_p * x_p, written in place over val[p] in the ring slot (val kept in registers)
+    //   B  one thread per row sums its products left to right, alpha = (f - s) / nrm2, and
+    //      broadcasts alpha over the row's entry slots
+    //   C  every thread scatters x_p + alpha * a_p for its entries (smem or L2), and the last
+    //      writer of a column adds (x - x*)^2 to the RSE partial
+    constexpr int NC = kNCW * 32;
+    const int cid = tid;
+    double acc_rse = 0.0;
+    long long sweep = 0, g = 0;
+    unsigned long long pf_go = 0, pf_full = 0, pf_bar = 0, pf_epoch = 0;
+    const unsigned long long pf_t0 = clock64();
+    while (sweep < maxs) {
+      acc_rse = 0.0;
+      for (int i = 0; i < nck; i++, g++) {
+        const int4 mt = cmeta[i];
+        const int rows = mt.x, nnz = mt.y, flags = mt.w;
+        unsigned long long pc0 = clock64();
+        if (flags & kFirstBoundary) {
+          const int jtask = (int)(sweep * ntask + mt.z);
+          while (ld_vol_shared(&ctl->go) <= jtask) {
+          }
+          __threadfence_block();
+        }
+        unsigned long long pc1 = clock64();
+        const int slot = (int)(g % kSlots);
+        mbar_wait(&ctl->full[slot], (unsigned)((g / kSlots) & 1));
+        unsigned long long pc2 = clock64();
+        pf_go += pc1 - pc0;
+        pf_full += pc2 - pc1;
+        unsigned char* blk = ring + slot * kChunkCap;
+        const ChunkLayout L(rows, nnz);
+        double* val = (double*)(blk + L.o_val);
+        const double* fv = (const double*)(blk + L.o_f);
+        const double* nv = (const double*)(blk + L.o_n);
+        const unsigned* col = (const unsigned*)(blk + L.o_col);
+        const int* rp = (const int*)(blk + L.o_rp);
+        unsigned cc[kEPT];
+        double av[kEPT], xv[kEPT];
+        // ---- A: gather and products
 #pragma unroll
-        for (int j = 0; j < KC; j++) {
-          const int p = p0 + lane + j * V;
-          cc[j] = p < p1 ? col[p] : 0u;
-          av[j] = p < p1 ? val[p] : 0.0;
+        for (int e = 0; e < kEPT; e++) {
+          const int p = cid + e * NC;
+          cc[e] = 0u;
+          av[e] = 0.0;
+          xv[e] = 0.0;
+          if (p < nnz) {
+            cc[e] = col[p];
+            av[e] = val[p];
+          }
         }
 #pragma unroll
-        for (int j = 0; j < KC; j++) {
-          const int p = p0 + lane + j * V;
-          const unsigned c = cc[j], idx = c & kIdx;
-          xv[j] = 0.0;
-          sv[j] = 0.0;
-          if (p < p1) {
+        for (int e = 0; e < kEPT; e++) {
+          const int p = cid + e * NC;
+          if (p < nnz) {
+            const unsigned c = cc[e], idx = c & kIdx;
             if (c & kShared) {
-              xv[j] = ld_cg(a.xg + idx);
-              if (c & kLast) sv[j] = __ldg(a.xst + idx);
+              xv[e] = ld_cg(a.xg + idx);
+              if (c & kLast) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.xst + idx));
             } else {
-              xv[j] = xloc[idx];
-              if (c & kLast) sv[j] = xsloc[idx];
+              xv[e] = xloc[idx];
             }
           }
         }
-        double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < KC; j++)
-          if (p0 + lane + j * V < p1) acc = fma(av[j], xv[j], acc);
-        for (int p = p0 + lane + KC * V; p < p1; p += V) {
-          const unsigned c = col[p];
-          acc = fma(val[p], (c & kShared) ? ld_cg(a.xg + (c & kIdx)) : xloc[c & kIdx], acc);
+        for (int e = 0; e < kEPT; e++) {
+          const int p = cid + e * NC;
+          if (p < nnz) val[p] = __dmul_rn(av[e], xv[e]);
         }
-        acc = vec_sum<V>(acc);
-        if (act) {
-          const double alpha = (fv[r] - acc) / nv[r];
+        named_bar(1, NC);
+        // ---- B: per-row sums (left to right), alpha, broadcast
+        for (int r = cid; r < rows; r += NC) {
+          const int p0 = rp[r], p1 = rp[r + 1];
+          double sum = 0.0;
+          for (int p = p0; p < p1; p++) sum = __dadd_rn(sum, val[p]);
+          const double alpha = __ddiv_rn(__dsub_rn(fv[r], sum), nv[r]);
+          for (int p = p0; p < p1; p++) val[p] = alpha;
+        }
+        named_bar(1, NC);
+        // ---- C: scatter
 #pragma unroll
-          for (int j = 0; j < KC; j++)
-            if (p0 + lane + j * V < p1) {
-              const unsigned c = cc[j], idx = c & kIdx;
-              const double xn = fma(alpha, av[j], xv[j]);
-              if (c & kShared) st_cg(a.xg + idx, xn);
-              else xloc[idx] = xn;
-              if (c & kLast) {
-                const double d = xn - sv[j];
-                acc_rse = fma(d, d, acc_rse);
-              }
-            }
-          for (int p = p0 + lane + KC * V; p < p1; p += V) {
-            const unsigned c = col[p], idx = c & kIdx;
-            const double xo = (c & kShared) ? ld_cg(a.xg + idx) : xloc[idx];
-            const double xn = fma(alpha, val[p], xo);
+        for (int e = 0; e < kEPT; e++) {
+          const int p = cid + e * NC;
+          if (p < nnz) {
+            const unsigned c = cc[e], idx = c & kIdx;
+            const double xn = __dadd_rn(xv[e], __dmul_rn(val[p], av[e]));
             if (c & kShared) st_cg(a.xg + idx, xn);
             else xloc[idx] = xn;
             if (c & kLast) {
@@ -285,69 +413,44 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             }
           }
         }
-      }
-      __syncthreads();  // slot free; the task's writes are complete before publishing
-      unsigned long long c_d = clock64();
-      if ((flags & kLastOfTask) && tid == 0) {
-        if (a.debug & 1) asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(a.progress + t * kFlagStride), "r"((int)(sweep * nsteps + mt.w)) : "memory");
-        else st_release(a.progress + t * kFlagStride, (int)(sweep * nsteps + mt.w));
-      }
-      if (a.prof && tid == 0) {
-        const unsigned long long c_e = clock64();
-        pr[0] += c_b - c_a; pr[1] += c_c - c_b; pr[2] += c_d - c_c; pr[3] += c_e - c_d;
-      }
-    }
-    const unsigned long long c_f = clock64();
-    sweep++;
-    const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
-    if (due) {
-      const double part = block_sum<kNT>(mode == POBK_STOP_RSE ? acc_rse : 0.0, red);
-      if (tid == 0) {
-        const int par = (int)(sweep & 1);
-        a.partials[par * a.T + t] = part;
-        __threadfence();
-        const unsigned old = atomicAdd(&a.sync->arrive[par], 1u);
-        if (old == (unsigned)a.T - 1) {
-          __threadfence();
-          double tot = 0.0;
-          for (int b = 0; b < a.T; b++) tot += ld_cg(a.partials + par * a.T + b);
-          const double v = sqrt(tot) / sqrt(den);
-          int stop = 0, term = POBK_TERM_MAX_SWEEPS;
-          if (!isfinite(v)) { stop = 1; term = POBK_TERM_NONFINITE; }
-          else if (v < tol) { stop = 1; term = POBK_TERM_CONVERGED; }
-          else if (sweep >= maxs) stop = 1;
-          a.sync->arrive[par] = 0;
-          a.sync->stop = stop;
-          a.ctrl->value = v;
-          a.ctrl->sweeps = sweep;
-          a.ctrl->term = term;
-          __threadfence();
-          st_release(&a.sync->epoch, (int)sweep);
-        } else {
-          while (ld_acquire(&a.sync->epoch) < (int)sweep) {
-          }
+        if ((flags & kLastOfTask) && i == nck - 1 && mode == POBK_STOP_RSE) {
+          // this warp's RSE partial (fixed lane order) before it reports the sweep's last task
+          double w = acc_rse;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+          if (wl == 0) ctl->part[warp] = w;
         }
-        s_stop = ld_relaxed(&a.sync->stop);
+        // generic-proxy writes to the slot (products, alphas) before the next TMA refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (wl == 0) {
+          __threadfence_block();
+          atomicAdd(&ctl->released[slot], 1);
+          if (flags & kLastOfTask) atomicAdd(&ctl->done, 1);
+        }
+        if (flags & kLastOfTask) {
+          const unsigned long long pb = clock64();
+          named_bar(1, NC);  // task k before task k+1 inside the tile
+          pf_bar += clock64() - pb;
+        }
       }
-      __syncthreads();
-      if (a.prof && tid == 0) pr[4] += clock64() - c_f;
-      if (s_stop) break;
-    } else if (sweep >= maxs) {
-      if (t == 0 && tid == 0) {
-        a.ctrl->sweeps = sweep;
-        a.ctrl->term = POBK_TERM_MAX_SWEEPS;
+      sweep++;
+      const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
+      if (due) {
+        const unsigned long long pe = clock64();
+        while (ld_vol_shared(&ctl->epoch) < (int)sweep) {
+        }
+        __threadfence_block();
+        pf_epoch += clock64() - pe;
+        if (ld_vol_shared(&ctl->stop)) break;
       }
-      break;
+    }
+    if (a.prof && tid == 0) {
+      unsigned long long* o = a.prof + t * 8;
+      o[0] = pf_go; o[1] = pf_full; o[2] = pf_bar; o[3] = pf_epoch; o[4] = clock64() - pf_t0; o[5] = nck;
     }
   }
-  if (a.prof && tid == 0) {
-    pr[5] = clock64() - t_start;
-    for (int j = 0; j < 6; j++) a.prof[t * 8 + j] = pr[j];
-    a.prof[t * 8 + 6] = (unsigned long long)nck;
-  }
-  // drain TMA copies issued ahead of the stop point, then write private x~ back
-  if (tid == 0)
-    for (long long h = g; h < issued; h++) mbar_wait(mbar + (int)(h % kSlots), (unsigned)((h / kSlots) & 1));
+  __syncthreads();
   for (int j = tid; j < np; j += kNT) a.xg[a.pmap[q0 + j]] = xloc[j];
 }
 
@@ -372,12 +475,14 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 struct K2Plan {
   int T = 0;
   size_t smem = 0;
-  int nck_max = 1, np_max = 1;
+  int nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
   long long* tile_off = nullptr;
   unsigned long long* prof = nullptr;
   ChunkMeta* meta = nullptr;
-  int *tile_chunk = nullptr, *nbr = nullptr, *pmap_ptr = nullptr, *pmap = nullptr, *k_first = nullptr;
+  TaskMeta* tmeta = nullptr;
+  int *tile_chunk = nullptr, *tile_task = nullptr, *nbr = nullptr, *pmap_ptr = nullptr, *pmap = nullptr;
+  int* k_first = nullptr;
   int* progress = nullptr;
   SyncState* sync = nullptr;
   double* partials = nullptr;
@@ -400,6 +505,7 @@ cudaError_t k2_upload(K2Plan& k, T** dst, const T* src, size_t n) {
   k.allocs.push_back(v);
   *dst = (T*)v;
   if (n && src) e = cudaMemcpy(v, src, n * sizeof(T), cudaMemcpyHostToDevice);
+  else if (n) e = cudaMemset(v, 0, n * sizeof(T));
   return e;
 }
 
@@ -443,9 +549,13 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       if (last_row[c] < 0 || step_of[i] > step_of[last_row[c]]) last_row[c] = (int32_t)i;
     }
   // private columns per tile (ascending), capped by shared memory
-  static_assert(kSlots <= 4, "mbarrier area holds 4");
-  const size_t fixed = (size_t)kSlots * kChunkCap + 4 * 8 + 32 * 8;
-  const int np_cap = (int)((kSmemLimit - 1024 - fixed - 20 * (size_t)kMaxChunks) / 16);  // x~ and x~* per column
+  const size_t fixed = (size_t)kSlots * kChunkCap + sizeof(Ctl) + 256;
+  const size_t meta_bytes = (size_t)20 * kMaxChunks + 16 * (size_t)p.nsteps;
+  if (fixed + meta_bytes + 16 * 1024 > (size_t)kSmemLimit - 1024) {
+    why = "too many schedule steps for K2's shared memory";
+    return false;
+  }
+  const int np_cap = (int)((kSmemLimit - 1024 - fixed - meta_bytes) / 16);  // x~ and x~* per column
   std::vector<int32_t> local(m, -1);
   std::vector<int> pmap_ptr(T + 1, 0);
   std::vector<int> pmap;
@@ -505,8 +615,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
     }
     n_interior += !boundary[i];
   }
-  // tasks and chunks, tile by tile
-  std::vector<std::vector<std::vector<int32_t>>> rows_tk(T);  // [t][k] rows (interior first)
+  // tasks and chunks, tile by tile (interior rows first within a task)
+  std::vector<std::vector<std::vector<int32_t>>> rows_tk(T);
   for (int t = 0; t < T; t++) rows_tk[t].resize(p.nsteps);
   for (int k = 0; k < p.nsteps; k++) {
     for (int pass = 0; pass < 2; pass++)
@@ -516,7 +626,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       }
   }
   std::vector<ChunkMeta> meta;
-  std::vector<int> tile_chunk(T + 1, 0), k_first(T, p.nsteps);
+  std::vector<TaskMeta> tmeta;
+  std::vector<int> tile_chunk(T + 1, 0), tile_task(T + 1, 0), k_first(T, p.nsteps);
   std::vector<std::vector<int32_t>> chunk_rows;
   for (int t = 0; t < T; t++) {
     std::vector<int> tasks;
@@ -525,17 +636,19 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
     if (!tasks.empty()) k_first[t] = tasks[0];
     for (size_t ti = 0; ti < tasks.size(); ti++) {
       const int k = tasks[ti];
-      const int k_next = ti + 1 < tasks.size() ? tasks[ti + 1] : p.nsteps + tasks[0];
+      TaskMeta tm{};
+      tm.step = k;
+      tm.k_next = ti + 1 < tasks.size() ? tasks[ti + 1] : p.nsteps + tasks[0];
+      tm.boundary = 0;
       const auto& rs = rows_tk[t][k];
       size_t a = 0;
-      bool first_boundary_done = false;
       while (a < rs.size()) {
         const uint8_t kind = boundary[rs[a]];
         size_t b = a;
         int nnz = 0;
         while (b < rs.size() && boundary[rs[b]] == kind) {
           const int len = (int)(At.ptr[rs[b] + 1] - At.ptr[rs[b]]);
-          if (ChunkLayout((int)(b - a + 1), nnz + len).bytes > kChunkCap) break;
+          if (ChunkLayout((int)(b - a + 1), nnz + len).bytes > kChunkCap || nnz + len > kEPT * kNCW * 32) break;
           nnz += len;
           b++;
         }
@@ -546,16 +659,18 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
         ChunkMeta mt{};
         mt.rows = (int)(b - a);
         mt.nnz = nnz;
-        mt.step = k;
+        mt.task = (int)ti;
         mt.flags = 0;
-        if (kind == 1 && !first_boundary_done) { mt.flags |= kFirstBoundary; first_boundary_done = true; }
-        if (b == rs.size()) { mt.flags |= kLastOfTask; mt.k_next = k_next; }
+        if (kind == 1 && !tm.boundary) { mt.flags |= kFirstBoundary; tm.boundary = 1; }
+        if (b == rs.size()) mt.flags |= kLastOfTask;
         meta.push_back(mt);
         chunk_rows.emplace_back(rs.begin() + a, rs.begin() + b);
         a = b;
       }
+      tmeta.push_back(tm);
     }
     tile_chunk[t + 1] = (int)meta.size();
+    tile_task[t + 1] = (int)tmeta.size();
     if (tile_chunk[t + 1] - tile_chunk[t] > kMaxChunks) {
       why = "tile " + std::to_string(t) + " needs more than " + std::to_string(kMaxChunks) + " chunks";
       return false;
@@ -606,11 +721,16 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   K2Plan* k = new K2Plan();
   p.k2 = k;
   k->T = T;
-  int nck_max = 1;
-  for (int t = 0; t < T; t++) nck_max = std::max(nck_max, tile_chunk[t + 1] - tile_chunk[t]);
+  int nck_max = 1, ntask_max = 1;
+  for (int t = 0; t < T; t++) {
+    nck_max = std::max(nck_max, tile_chunk[t + 1] - tile_chunk[t]);
+    ntask_max = std::max(ntask_max, tile_task[t + 1] - tile_task[t]);
+  }
   k->nck_max = nck_max;
+  k->ntask_max = ntask_max;
   k->np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
-  k->smem = fixed + 16 * (size_t)nck_max + 4 * (size_t)((nck_max + 3) & ~3) + 16 * (size_t)k->np_max;
+  k->smem = fixed + 16 * (size_t)nck_max + 4 * (size_t)((nck_max + 3) & ~3) + 16 * (size_t)ntask_max +
+            16 * (size_t)k->np_max;
   std::vector<long long> tile_off(T, 0);
   for (int t = 0; t < T; t++) tile_off[t] = tile_chunk[t] < (int)meta.size() ? meta[tile_chunk[t]].off : 0;
   k->private_frac = p.nnz ? (double)n_private_nnz / (double)p.nnz : 0.0;
@@ -623,7 +743,9 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   K2_UP(&k->stream, stream.data(), stream.size());
   K2_UP(&k->tile_off, tile_off.data(), tile_off.size());
   K2_UP(&k->meta, meta.data(), meta.size());
+  K2_UP(&k->tmeta, tmeta.data(), tmeta.size());
   K2_UP(&k->tile_chunk, tile_chunk.data(), tile_chunk.size());
+  K2_UP(&k->tile_task, tile_task.data(), tile_task.size());
   K2_UP(&k->nbr, nbr.data(), nbr.size());
   K2_UP(&k->pmap_ptr, pmap_ptr.data(), pmap_ptr.size());
   K2_UP(&k->pmap, pmap.data(), pmap.size());
@@ -654,22 +776,13 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   K2Args a;
   a.stream = k.stream;
   a.tile_off = k.tile_off;
-  a.nck_max = k.nck_max;
-  a.prof = nullptr;
-  static const int dbg = getenv("POBK_K2_DEBUG") ? atoi(getenv("POBK_K2_DEBUG")) : 0;
-  a.debug = dbg;
-  static const bool prof_on = getenv("POBK_K2_PROFILE") != nullptr;
-  if (prof_on) {
-    if (!k.prof) cudaMalloc(&k.prof, (size_t)k.T * 8 * sizeof(unsigned long long));
-    a.prof = k.prof;
-  }
-  a.np_max = k.np_max;
   a.meta = k.meta;
   a.tile_chunk = k.tile_chunk;
+  a.tmeta = k.tmeta;
+  a.tile_task = k.tile_task;
   a.nbr = k.nbr;
   a.pmap_ptr = k.pmap_ptr;
   a.pmap = k.pmap;
-  a.k_first = k.k_first;
   a.xg = p.d_xt;
   a.xst = p.d_xst;
   a.progress = k.progress;
@@ -678,16 +791,20 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.ctrl = p.d_ctrl;
   a.nsteps = p.nsteps;
   a.T = k.T;
-  void* args[] = {&a};
-  const void* fn = nullptr;
-  switch (p.V) {
-    case 1: fn = (const void*)k2_sweeps<1>; break;
-    case 2: fn = (const void*)k2_sweeps<2>; break;
-    case 4: fn = (const void*)k2_sweeps<4>; break;
-    case 8: fn = (const void*)k2_sweeps<8>; break;
-    case 16: fn = (const void*)k2_sweeps<16>; break;
-    default: fn = (const void*)k2_sweeps<32>; break;
+  a.nck_max = k.nck_max;
+  a.ntask_max = k.ntask_max;
+  a.np_max = k.np_max;
+  static const int dbg = getenv("POBK_K2_DEBUG") ? atoi(getenv("POBK_K2_DEBUG")) : 0;
+  a.debug = dbg;
+  a.prof = nullptr;
+  static const bool prof_on = getenv("POBK_K2_PROFILE") != nullptr;
+  if (prof_on) {
+    if (!k.prof) cudaMalloc(&k.prof, (size_t)k.T * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(k.prof, 0, (size_t)k.T * 8 * sizeof(unsigned long long), s);
+    a.prof = k.prof;
   }
+  void* args[] = {&a};
+  const void* fn = (const void*)k2_sweeps;
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(kNT), args, k.smem, s);
   launches++;
@@ -695,13 +812,13 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     std::vector<unsigned long long> h((size_t)k.T * 8);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    double sum[7] = {0}, mx[7] = {0};
+    double sum[6] = {0}, mx[6] = {0};
     for (int t = 0; t < k.T; t++)
-      for (int j = 0; j < 7; j++) { sum[j] += (double)h[t * 8 + j]; mx[j] = std::max(mx[j], (double)h[t * 8 + j]); }
-    fprintf(stderr, "[k2 prof] cycles per tile (mean / max): nbwait %.3g/%.3g mbarwait %.3g/%.3g compute %.3g/%.3g "
-                    "publish %.3g/%.3g barrier %.3g/%.3g total %.3g/%.3g chunks %.0f\n",
+      for (int j = 0; j < 6; j++) { sum[j] += (double)h[t * 8 + j]; mx[j] = std::max(mx[j], (double)h[t * 8 + j]); }
+    fprintf(stderr, "[k2 prof] warp0 cycles per tile (mean/max): go %.3g/%.3g full %.3g/%.3g taskbar %.3g/%.3g "
+                    "epoch %.3g/%.3g total %.3g/%.3g chunks %.0f\n",
             sum[0] / k.T, mx[0], sum[1] / k.T, mx[1], sum[2] / k.T, mx[2], sum[3] / k.T, mx[3], sum[4] / k.T, mx[4],
-            sum[5] / k.T, mx[5], sum[6] / k.T);
+            sum[5] / k.T);
   }
   return e;
 }
@@ -714,9 +831,6 @@ void k2_free(Plan& p) {
   p.k2 = nullptr;
 }
 
-}  // namespace pobk
-
-namespace pobk {
 bool k2_stats(const Plan& p, K2Stats& st) {
   if (!p.k2) return false;
   st.T = p.k2->T;
@@ -726,4 +840,5 @@ bool k2_stats(const Plan& p, K2Stats& st) {
   st.nchunks = p.k2->nchunks;
   return true;
 }
+
 }  // namespace pobk

@@ -1,6 +1,6 @@
 // K3: the whole system resident in one CTA's shared memory (small systems, e.g. BASELINE config 1:
 // m = 1024, 4,992 nnz, ~97 KB).  One launch runs every sweep: per schedule step the CTA's
-// V-lane vectors project their rows (Eq 1.2, per the contract in common.cuh),
+// threads project one row each (Eq 1.2, per the contract in common.cuh),
 // __syncthreads() is the step barrier, and after every due sweep a deterministic block reduction
 // evaluates the stop rule.  Latency-bound by design: ~nsteps barriers per sweep,
 // no global-memory traffic inside the loop.
@@ -35,7 +35,6 @@ __host__ __device__ inline size_t k3_bytes(int m, int nnz, int nsteps, int max_o
          align16(4ull * nnz) + align16(4ull * (m + 1)) + align16(4ull * (nsteps + 1)) + align16(nsteps) + 64 * 8;
 }
 
-template <int V>
 __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* q = smem;
@@ -70,7 +69,6 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
   if (tid == 0) s_stop = maxs <= 0;
   __syncthreads();
 
-  const int lane = tid % V, vec = tid / V, nvec = kNT / V;
   long long sweep = 0;
   double value = NAN;
   int term = POBK_TERM_MAX_SWEEPS;
@@ -78,34 +76,13 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
     for (int k = 0; k < a.nsteps; k++) {
       const int s0 = sp[k], s1 = sp[k + 1];
       if (!ov[k]) {
-        for (int base = s0; base < s1; base += nvec) {
-          const int s = base + vec;
-          const bool act = s < s1;
-          const int p0 = act ? rp[s] : 0, p1 = act ? rp[s + 1] : 0;
-          double acc = 0.0;
-          for (int p = p0 + lane; p < p1; p += V) acc = fma(val[p], x[col[p]], acc);
-          acc = vec_sum<V>(acc);
-          if (act) {
-            const double al = (f[s] - acc) / nrm2[s];
-            for (int p = p0 + lane; p < p1; p += V) x[col[p]] = fma(al, val[p], x[col[p]]);
-          }
-        }
+        for (int s = s0 + tid; s < s1; s += kNT) row_project(col, val, rp[s], rp[s + 1], f[s], nrm2[s], x);
       } else {
-        for (int base = s0; base < s1; base += nvec) {
-          const int s = base + vec;
-          const bool act = s < s1;
-          const int p0 = act ? rp[s] : 0, p1 = act ? rp[s + 1] : 0;
-          double acc = 0.0;
-          for (int p = p0 + lane; p < p1; p += V) acc = fma(val[p], x[col[p]], acc);
-          acc = vec_sum<V>(acc);
-          if (act && lane == 0) alpha[s - s0] = (f[s] - acc) / nrm2[s];
-        }
+        for (int s = s0 + tid; s < s1; s += kNT)
+          alpha[s - s0] = __ddiv_rn(__dsub_rn(f[s], row_dot(col, val, rp[s], rp[s + 1], x)), nrm2[s]);
         __syncthreads();
-        for (int base = s0; base < s1; base += nvec) {
-          const int s = base + vec;
-          if (s < s1)
-            for (int p = rp[s] + lane; p < rp[s + 1]; p += V) atomicAdd(x + col[p], alpha[s - s0] * val[p]);
-        }
+        for (int s = s0 + tid; s < s1; s += kNT)
+          for (int p = rp[s]; p < rp[s + 1]; p++) atomicAdd(x + col[p], __dmul_rn(alpha[s - s0], val[p]));
       }
       __syncthreads();
     }
@@ -116,14 +93,9 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
       if (mode == POBK_STOP_RSE) {
         for (int i = tid; i < a.m; i += kNT) { const double d = x[i] - xs[i]; loc = fma(d, d, loc); }
       } else {
-        for (int base = 0; base < a.m; base += nvec) {
-          const int s = base + vec;
-          const bool act = s < a.m;
-          const int p0 = act ? rp[s] : 0, p1 = act ? rp[s + 1] : 0;
-          double acc = 0.0;
-          for (int p = p0 + lane; p < p1; p += V) acc = fma(val[p], x[col[p]], acc);
-          acc = vec_sum<V>(acc);
-          if (act && lane == 0) { const double r = f[s] - acc; loc = fma(r, r, loc); }
+        for (int s = tid; s < a.m; s += kNT) {
+          const double r = __dsub_rn(f[s], row_dot(col, val, rp[s], rp[s + 1], x));
+          loc = fma(r, r, loc);
         }
       }
       const double tot = block_sum<kNT>(loc, red);
@@ -152,7 +124,6 @@ int max_overlap_step(const Plan& p) {
   return mx;
 }
 
-template <int V>
 cudaError_t launch(Plan& p, cudaStream_t s) {
   K3Args a;
   a.m = (int)p.m;
@@ -169,9 +140,9 @@ cudaError_t launch(Plan& p, cudaStream_t s) {
   a.xt = p.d_xt;
   a.xst = p.d_xst;
   a.ctrl = p.d_ctrl;
-  cudaError_t e = cudaFuncSetAttribute(k3_sweeps<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+  cudaError_t e = cudaFuncSetAttribute(k3_sweeps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
   if (e != cudaSuccess) return e;
-  k3_sweeps<V><<<1, kNT, p.k3_smem, s>>>(a);
+  k3_sweeps<<<1, kNT, p.k3_smem, s>>>(a);
   return cudaGetLastError();
 }
 }  // namespace
@@ -184,14 +155,7 @@ bool k3_fits(const Plan& p, size_t& bytes) {
 
 cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches) {
   launches++;
-  switch (p.V) {
-    case 1: return launch<1>(p, s);
-    case 2: return launch<2>(p, s);
-    case 4: return launch<4>(p, s);
-    case 8: return launch<8>(p, s);
-    case 16: return launch<16>(p, s);
-    default: return launch<32>(p, s);
-  }
+  return launch(p, s);
 }
 
 }  // namespace pobk

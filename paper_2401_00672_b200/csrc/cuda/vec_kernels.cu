@@ -44,36 +44,25 @@ __global__ void k_permute_out(int64_t m, const int32_t* __restrict__ perm, const
 }
 
 // Sum of squares of row residuals over storage rows [b*chunk, (b+1)*chunk) of this block,
-// optionally restricted to user-frame rows [lo, hi).
-template <int V>
+// optionally restricted to user-frame rows [lo, hi).  One thread per row, the row's dot product
+// in the contract's order (common.cuh), squares accumulated per thread in a fixed order.
 __device__ double residual_chunk(int64_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                  const double* __restrict__ val, const double* __restrict__ fs,
                                  const double* __restrict__ xt, const int32_t* __restrict__ orig, int64_t lo,
                                  int64_t hi) {
   const int64_t chunk = (m + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * chunk, b1 = min(m, b0 + chunk);
-  const int lane = threadIdx.x % V, vec = threadIdx.x / V, nvec = blockDim.x / V;
   double acc = 0.0;
-  for (int64_t base = b0; base < b1; base += nvec) {
-    const int64_t s = base + vec;
-    double d = 0.0;
-    if (s < b1)
-      for (int p = rp[s] + lane; p < rp[s + 1]; p += V) d = fma(val[p], ld_cg(xt + col[p]), d);
-    d = vec_sum<V>(d);
-    if (s < b1 && lane == 0) {
-      const bool in = !orig || (orig[s] >= lo && orig[s] < hi);
-      if (in) {
-        const double r = fs[s] - d;
-        acc = fma(r, r, acc);
-      }
-    }
+  for (int64_t s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
+    if (orig && (orig[s] < lo || orig[s] >= hi)) continue;
+    const double r = __dsub_rn(fs[s], row_dot(col, val, rp[s], rp[s + 1], xt));
+    acc = fma(r, r, acc);
   }
   return acc;
 }
 
 // The per-sweep stop check (K5, or K4 for RELRES).  Runs as the last node of every K1 sweep and
 // after every K2/K3 sweep is NOT needed (those kernels check internally).
-template <int V>
 __global__ void __launch_bounds__(kNT) k_check(Ctrl* __restrict__ c, int64_t m, const double* __restrict__ xt,
                                                const double* __restrict__ xst, const int32_t* __restrict__ rp,
                                                const int32_t* __restrict__ col, const double* __restrict__ val,
@@ -94,7 +83,7 @@ __global__ void __launch_bounds__(kNT) k_check(Ctrl* __restrict__ c, int64_t m, 
         local = fma(d, d, local);
       }
     } else {
-      local = residual_chunk<V>(m, rp, col, val, fs, xt, nullptr, 0, 0);
+      local = residual_chunk(m, rp, col, val, fs, xt, nullptr, 0, 0);
     }
   }
   const double bs = block_sum<kNT>(local, sh);
@@ -147,7 +136,6 @@ __global__ void __launch_bounds__(kNT) k_den(Ctrl* __restrict__ c, int64_t m, co
   c->den = tot;
 }
 
-template <int V>
 __global__ void __launch_bounds__(kNT) k_resid(int64_t m, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ fs,
                                                const double* __restrict__ xt, const int32_t* __restrict__ orig,
@@ -155,7 +143,7 @@ __global__ void __launch_bounds__(kNT) k_resid(int64_t m, const int32_t* __restr
                                                unsigned int* __restrict__ arrive, double* __restrict__ out) {
   __shared__ double sh[kNT / 32];
   __shared__ int is_last;
-  const double bs = block_sum<kNT>(residual_chunk<V>(m, rp, col, val, fs, xt, orig, lo, hi), sh);
+  const double bs = block_sum<kNT>(residual_chunk(m, rp, col, val, fs, xt, orig, lo, hi), sh);
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = bs;
     __threadfence();
@@ -213,33 +201,16 @@ cudaError_t launch_init_ctrl(const Plan& p, const pobk_solve_opts& o, cudaStream
   return cudaGetLastError();
 }
 
-template <int V>
-static cudaError_t launch_check_v(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h, int use_h) {
-  k_check<V><<<reduce_blocks(p.m), kNT, 0, s>>>(p.d_ctrl, p.m, p.d_xt, p.d_xst, p.A.rp, p.A.col, p.A.val, p.d_fs,
-                                                 p.d_partials, h, use_h);
+cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h) {
+  k_check<<<reduce_blocks(p.m), kNT, 0, s>>>(p.d_ctrl, p.m, p.d_xt, p.d_xst, p.A.rp, p.A.col, p.A.val, p.d_fs,
+                                             p.d_partials, h, 1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h) {
-  switch (p.V) {
-    case 1: return launch_check_v<1>(p, s, h, 1);
-    case 2: return launch_check_v<2>(p, s, h, 1);
-    case 4: return launch_check_v<4>(p, s, h, 1);
-    case 8: return launch_check_v<8>(p, s, h, 1);
-    case 16: return launch_check_v<16>(p, s, h, 1);
-    default: return launch_check_v<32>(p, s, h, 1);
-  }
-}
-
 cudaError_t launch_check(const Plan& p, cudaStream_t s) {
-  switch (p.V) {
-    case 1: return launch_check_v<1>(p, s, 0, 0);
-    case 2: return launch_check_v<2>(p, s, 0, 0);
-    case 4: return launch_check_v<4>(p, s, 0, 0);
-    case 8: return launch_check_v<8>(p, s, 0, 0);
-    case 16: return launch_check_v<16>(p, s, 0, 0);
-    default: return launch_check_v<32>(p, s, 0, 0);
-  }
+  k_check<<<reduce_blocks(p.m), kNT, 0, s>>>(p.d_ctrl, p.m, p.d_xt, p.d_xst, p.A.rp, p.A.col, p.A.val, p.d_fs,
+                                             p.d_partials, 0, 0);
+  return cudaGetLastError();
 }
 
 cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, const int32_t* orig, int64_t lo,
@@ -251,14 +222,7 @@ cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, co
   cudaError_t e = cudaMemsetAsync(arrive, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   const int B = reduce_blocks(p.m);
-  switch (p.V) {
-    case 1: k_resid<1><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-    case 2: k_resid<2><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-    case 4: k_resid<4><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-    case 8: k_resid<8><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-    case 16: k_resid<16><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-    default: k_resid<32><<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out); break;
-  }
+  k_resid<<<B, kNT, 0, s>>>(p.m, p.A.rp, p.A.col, p.A.val, fs, xt, orig, lo, hi, p.d_partials, arrive, out);
   launches++;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemcpyAsync(host_out, out, sizeof(double), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;

@@ -30,7 +30,6 @@ struct Plan {
   double prep_seconds = 0.0;
   double thr = 0.0;
   int kernel = POBK_KERNEL_AUTO;  // family chosen at preprocess
-  int V = 4;                      // lanes per row (fixes the per-row summation tree for every kernel)
   bool any_overlap = false;
 
   // host copies (queries, tests)

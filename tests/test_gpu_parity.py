@@ -62,12 +62,14 @@ def test_fixed_sweeps_parity(env, name, n, kernel):
     _, x, rep = _run(env, s, nf, plan=plan)
     ref = O.run_sweeps(pre, s.f, nf)
     assert _rel(x, ref) <= REL, (rep.as_dict(), _rel(x, ref))
+    assert np.array_equal(x, ref), "thr = 0 iterates are bitwise the oracle's (common.cuh contract)"
 
 
 @pytest.mark.parametrize("name,n", [("lap2d5_32", None), ("lap3d7_64", 11), ("randband_20k", 3000),
                                     ("geoknn_1m", 120000)])
 def test_kernel_families_bitwise_equal(env, name, n):
-    """Same per-row arithmetic contract (common.cuh) -> bitwise-identical iterates (T3)."""
+    """Same per-row arithmetic contract (common.cuh) -> bitwise-identical iterates (T3), and -- since
+    the contract is the oracle's own operation order -- bitwise equal to the oracle (thr = 0)."""
     pk, _ = env
     s = gen.make(name, n=n) if n else gen.make(name)
     outs = {}
@@ -80,6 +82,8 @@ def test_kernel_families_bitwise_equal(env, name, n):
     vals = list(outs.values())
     for v in vals[1:]:
         assert np.array_equal(v, vals[0]), list(outs)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    assert np.array_equal(vals[0], O.run_sweeps(pre, s.f, 12))
 
 
 def test_repeatable_bitwise(env):
