@@ -40,15 +40,25 @@
 namespace pobk {
 
 namespace {
-constexpr int kNT = 1024;           // threads per CTA
-constexpr int kNCW = 31;            // compute warps (warp 31 = control)
+#ifndef POBK_K2_CPS
+#define POBK_K2_CPS 1
+#endif
+constexpr int kCPS = POBK_K2_CPS;   // CTAs (tiles) per SM
+#ifndef POBK_K2_NT
+#define POBK_K2_NT 1024
+#endif
+constexpr int kNT = POBK_K2_NT / kCPS;  // threads per CTA
+constexpr int kNCW = kNT / 32 - 1;  // compute warps (the last warp = control)
 constexpr int kSlots = 3;           // TMA ring depth
-constexpr int kChunkCap = 40 * 1024;
-constexpr int kEPT = 4;             // entries per compute thread per chunk (chunk nnz <= kEPT * 992)
-constexpr int kNbMax = 16;          // max neighbour tiles
+constexpr int kChunkCap = 40 * 1024 / kCPS;
+#ifndef POBK_K2_EPT
+#define POBK_K2_EPT 4
+#endif
+constexpr int kEPT = POBK_K2_EPT;   // entries per compute thread per chunk (chunk nnz <= kEPT * compute threads)
+constexpr int kNbMax = 32;          // max neighbour tiles (one control-warp lane each)
 constexpr int kMaxChunks = 1024;    // max chunks per tile (metadata lives in shared memory)
 constexpr int kFlagStride = 32;     // ints between progress counters (one 128-B line each)
-constexpr int kSmemLimit = 227 * 1024;
+constexpr int kSmemLimit = 228 * 1024 / kCPS - 1024;
 constexpr unsigned kShared = 0x80000000u, kLast = 0x40000000u, kIdx = 0x3FFFFFFFu;
 constexpr int kFirstBoundary = 1, kLastOfTask = 2;
 
@@ -152,7 +162,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-__global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
+__global__ void __launch_bounds__(kNT, kCPS) k2_sweeps(K2Args a) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;                                   // kSlots * kChunkCap
   Ctl* ctl = (Ctl*)(smem + kSlots * kChunkCap);
@@ -330,6 +340,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     double acc_rse = 0.0;
     long long sweep = 0, g = 0;
     unsigned long long pf_go = 0, pf_full = 0, pf_bar = 0, pf_epoch = 0;
+    unsigned long long pf_a = 0, pf_ab = 0, pf_b = 0, pf_bb = 0, pf_c = 0;
     const unsigned long long pf_t0 = clock64();
     while (sweep < maxs) {
       acc_rse = 0.0;
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         const unsigned* col = (const unsigned*)(blk + L.o_col);
         const int* rp = (const int*)(blk + L.o_rp);
         unsigned cc[kEPT];
-        double av[kEPT], xv[kEPT];
+        double av[kEPT], xv[kEPT], sv[kEPT];
         // ---- A: gather and products
 #pragma unroll
         for (int e = 0; e < kEPT; e++) {
@@ -365,6 +376,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           cc[e] = 0u;
           av[e] = 0.0;
           xv[e] = 0.0;
+          sv[e] = 0.0;
           if (p < nnz) {
             cc[e] = col[p];
             av[e] = val[p];
@@ -377,9 +389,10 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             const unsigned c = cc[e], idx = c & kIdx;
             if (c & kShared) {
               xv[e] = ld_cg(a.xg + idx);
-              if (c & kLast) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.xst + idx));
+              if (c & kLast) sv[e] = __ldg(a.xst + idx);
             } else {
               xv[e] = xloc[idx];
+              if (c & kLast) sv[e] = xsloc[idx];
             }
           }
         }
@@ -388,16 +401,28 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           const int p = cid + e * NC;
           if (p < nnz) val[p] = __dmul_rn(av[e], xv[e]);
         }
+        unsigned long long pA = clock64();
         named_bar(1, NC);
+        unsigned long long pA2 = clock64();
         // ---- B: per-row sums (left to right), alpha, broadcast
         for (int r = cid; r < rows; r += NC) {
           const int p0 = rp[r], p1 = rp[r + 1];
           double sum = 0.0;
-          for (int p = p0; p < p1; p++) sum = __dadd_rn(sum, val[p]);
+          int p = p0;
+          for (; p + 8 <= p1; p += 8) {  // batch the loads, keep the left-to-right additions
+            double v[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) v[j] = val[p + j];
+#pragma unroll
+            for (int j = 0; j < 8; j++) sum = __dadd_rn(sum, v[j]);
+          }
+          for (; p < p1; p++) sum = __dadd_rn(sum, val[p]);
           const double alpha = __ddiv_rn(__dsub_rn(fv[r], sum), nv[r]);
-          for (int p = p0; p < p1; p++) val[p] = alpha;
+          for (p = p0; p < p1; p++) val[p] = alpha;
         }
+        unsigned long long pB = clock64();
         named_bar(1, NC);
+        unsigned long long pB2 = clock64();
         // ---- C: scatter
 #pragma unroll
         for (int e = 0; e < kEPT; e++) {
@@ -408,11 +433,13 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             if (c & kShared) st_cg(a.xg + idx, xn);
             else xloc[idx] = xn;
             if (c & kLast) {
-              const double d = xn - ((c & kShared) ? __ldg(a.xst + idx) : xsloc[idx]);
+              const double d = xn - sv[e];
               acc_rse = fma(d, d, acc_rse);
             }
           }
         }
+        unsigned long long pC = clock64();
+        pf_a += pA - pc2; pf_ab += pA2 - pA; pf_b += pB - pA2; pf_bb += pB2 - pB; pf_c += pC - pB2;
         if ((flags & kLastOfTask) && i == nck - 1 && mode == POBK_STOP_RSE) {
           // this warp's RSE partial (fixed lane order) before it reports the sweep's last task
           double w = acc_rse;
@@ -446,8 +473,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       }
     }
     if (a.prof && tid == 0) {
-      unsigned long long* o = a.prof + t * 8;
+      unsigned long long* o = a.prof + t * 16;
       o[0] = pf_go; o[1] = pf_full; o[2] = pf_bar; o[3] = pf_epoch; o[4] = clock64() - pf_t0; o[5] = nck;
+      o[6] = pf_a; o[7] = pf_ab; o[8] = pf_b; o[9] = pf_bb; o[10] = pf_c;
     }
   }
   __syncthreads();
@@ -509,15 +537,88 @@ cudaError_t k2_upload(K2Plan& k, T** dst, const T* src, size_t n) {
   return e;
 }
 
-// 1-D tiler: contiguous RCM row ranges with equal nnz.
-void tile_1d(const HostCSR& A, int T, std::vector<int32_t>& tile_of_row) {
+// Tilers.  Tiles only change WHERE rows run, never the result.
+//
+// 2-D tiler: S slabs of consecutive RCM rows (equal nnz); inside a slab -- a band of consecutive
+// BFS fronts -- rows are ordered by their BFS distance from a far end of the slab's own graph
+// (the direction ALONG the fronts) and cut into P pieces of equal nnz.  On mesh-like matrices this
+// yields compact patches, so far fewer x~ columns are shared between tiles than with 1-D ranges.
+// S = T, P = 1 is the plain 1-D tiling.
+void tile_2d(const HostCSR& A, int S, int P, std::vector<int32_t>& tile_of_row) {
   const int64_t m = A.m, nnz = A.nnz();
-  tile_of_row.resize(m);
-  int t = 0;
-  for (int64_t i = 0; i < m; i++) {
-    while (t < T - 1 && A.ptr[i] >= (int64_t)((double)nnz * (t + 1) / T)) t++;
-    tile_of_row[i] = t;
+  tile_of_row.assign(m, 0);
+  std::vector<int64_t> cut(S + 1, m);
+  cut[0] = 0;
+  {
+    int s = 0;
+    for (int64_t i = 0; i < m && s < S - 1; i++)
+      while (s < S - 1 && A.ptr[i] >= (int64_t)((double)nnz * (s + 1) / S)) cut[++s] = i;
+    for (int k = s + 1; k < S; k++) cut[k] = m;
   }
+  std::vector<int32_t> dist(m, -1), q;
+  for (int s = 0; s < S; s++) {
+    const int64_t b = cut[s], e = std::max(cut[s], cut[s + 1]);
+    if (e <= b) continue;
+    if (P == 1) {
+      for (int64_t i = b; i < e; i++) tile_of_row[i] = s;
+      continue;
+    }
+    auto bfs = [&](int32_t src, int32_t base) -> int32_t {  // returns the last node reached
+      q.clear();
+      q.push_back(src);
+      dist[src] = base;
+      size_t h = 0;
+      int32_t last = src;
+      while (h < q.size()) {
+        const int32_t v = q[h++];
+        last = v;
+        for (int64_t k = A.ptr[v]; k < A.ptr[v + 1]; k++) {
+          const int32_t u = A.col[k];
+          if (u >= b && u < e && dist[u] < 0) { dist[u] = dist[v] + 1; q.push_back(u); }
+        }
+      }
+      return last;
+    };
+    // far end: BFS from the slab's first row, restart from the farthest node
+    int32_t far = bfs((int32_t)b, 0);
+    for (int64_t i = b; i < e; i++) dist[i] = -1;
+    int32_t base = 0;
+    bfs(far, 0);
+    for (int64_t i = b; i < e; i++)  // other components of the slab continue the ordering
+      if (dist[i] < 0) {
+        int32_t mx = 0;
+        for (int64_t j = b; j < e; j++) mx = std::max(mx, dist[j]);
+        base = mx + 1;
+        bfs((int32_t)i, base);
+      }
+    std::vector<int32_t> ord(e - b);
+    std::iota(ord.begin(), ord.end(), (int32_t)b);
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return dist[x] < dist[y]; });
+    int64_t slab_nnz = A.ptr[e] - A.ptr[b], acc = 0;
+    int piece = 0;
+    for (int32_t r : ord) {
+      while (piece < P - 1 && acc >= (int64_t)((double)slab_nnz * (piece + 1) / P)) piece++;
+      tile_of_row[r] = s * P + piece;
+      acc += A.ptr[r + 1] - A.ptr[r];
+    }
+    for (int64_t i = b; i < e; i++) dist[i] = -1;
+  }
+}
+
+// fraction of nonzeros whose column is touched by one tile only
+double private_fraction(const HostCSR& A, const std::vector<int32_t>& tile) {
+  const int64_t m = A.m;
+  std::vector<int32_t> ct(m, -1);
+  std::vector<uint8_t> sh(m, 0);
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t k = A.ptr[i]; k < A.ptr[i + 1]; k++) {
+      const int32_t c = A.col[k];
+      if (ct[c] < 0) ct[c] = tile[i];
+      else if (ct[c] != tile[i]) sh[c] = 1;
+    }
+  int64_t priv = 0;
+  for (int64_t k = 0; k < A.nnz(); k++) priv += !sh[A.col[k]];
+  return A.nnz() ? (double)priv / (double)A.nnz() : 1.0;
 }
 }  // namespace
 
@@ -527,11 +628,31 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, p.device) == cudaSuccess) sms = prop.multiProcessorCount;
   const int64_t m = p.m;
-  int T = sms;
-  if (tile_rows > 0) T = (int)std::max<int64_t>(1, std::min<int64_t>(sms, (m + tile_rows - 1) / tile_rows));
+  int T = sms * kCPS;
+  if (tile_rows > 0) T = (int)std::max<int64_t>(1, std::min<int64_t>(T, (m + tile_rows - 1) / tile_rows));
   T = (int)std::min<int64_t>(T, std::max<int64_t>(1, p.nnz / 4096));
+  // tiling: among T' in {T, T-4, T-8} (one tile per SM, a few SMs may idle) and the factorisations
+  // T' = S x P, the one with the best (private fraction - load penalty); S = T' is the 1-D tiling
   std::vector<int32_t> tile;
-  tile_1d(At, T, tile);
+  {
+    double best = -1e9;
+    int bestT = T;
+    const char* force = getenv("POBK_K2_SLABS");  // development override of S
+    for (int Tc : {T, T - 4, T - 8}) {
+      if (Tc < 1) continue;
+      for (int S = 1; S <= Tc; S++) {
+        if (Tc % S) continue;
+        if (force ? S != atoi(force) : (S != Tc && (S < 2 || Tc / S < 2))) continue;
+        std::vector<int32_t> cand;
+        tile_2d(At, S, Tc / S, cand);
+        const double score = private_fraction(At, cand) - 1.5 * (1.0 - (double)Tc / T);
+        if (score > best) { best = score; tile.swap(cand); bestT = Tc; }
+      }
+      if (force) break;
+    }
+    if (tile.empty()) tile_2d(At, T, 1, tile);
+    T = bestT;
+  }
 
   // step of every RCM row
   std::vector<int32_t> step_of(m);
@@ -799,8 +920,8 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.prof = nullptr;
   static const bool prof_on = getenv("POBK_K2_PROFILE") != nullptr;
   if (prof_on) {
-    if (!k.prof) cudaMalloc(&k.prof, (size_t)k.T * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(k.prof, 0, (size_t)k.T * 8 * sizeof(unsigned long long), s);
+    if (!k.prof) cudaMalloc(&k.prof, (size_t)k.T * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(k.prof, 0, (size_t)k.T * 16 * sizeof(unsigned long long), s);
     a.prof = k.prof;
   }
   void* args[] = {&a};
@@ -809,12 +930,14 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(kNT), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.prof) {
-    std::vector<unsigned long long> h((size_t)k.T * 8);
+    std::vector<unsigned long long> h((size_t)k.T * 16);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    double sum[6] = {0}, mx[6] = {0};
+    double sum[11] = {0}, mx[11] = {0};
     for (int t = 0; t < k.T; t++)
-      for (int j = 0; j < 6; j++) { sum[j] += (double)h[t * 8 + j]; mx[j] = std::max(mx[j], (double)h[t * 8 + j]); }
+      for (int j = 0; j < 11; j++) { sum[j] += (double)h[t * 16 + j]; mx[j] = std::max(mx[j], (double)h[t * 16 + j]); }
+    fprintf(stderr, "[k2 prof] phases (mean per tile): A %.3g barA %.3g B %.3g barB %.3g C %.3g\n", sum[6] / k.T,
+            sum[7] / k.T, sum[8] / k.T, sum[9] / k.T, sum[10] / k.T);
     fprintf(stderr, "[k2 prof] warp0 cycles per tile (mean/max): go %.3g/%.3g full %.3g/%.3g taskbar %.3g/%.3g "
                     "epoch %.3g/%.3g total %.3g/%.3g chunks %.0f\n",
             sum[0] / k.T, mx[0], sum[1] / k.T, mx[1], sum[2] / k.T, mx[2], sum[3] / k.T, mx[3], sum[4] / k.T, mx[4],
