@@ -256,13 +256,9 @@ def main():
     err = max(float(np.linalg.norm(x.cpu().numpy() - s.x_star) / np.linalg.norm(s.x_star)) for x, s in zip(xs, systems))
 
     if world > 1:
-        buf = torch.tensor([t, t_e2e, updates, e2e_updates, sweep_t], dtype=torch.float64, device=dev)
-        mx = buf.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = buf.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        t, t_e2e, sweep_t = mx[0].item(), mx[1].item(), mx[4].item()
-        updates, e2e_updates = sm[2].item(), sm[3].item()
+        from paper_2401_00672_b200 import driver
+        t, t_e2e, sweep_t = (driver.max_over_ranks(v, dev) for v in (t, t_e2e, sweep_t))
+        updates, e2e_updates = (driver.sum_over_ranks(v, dev) for v in (updates, e2e_updates))
     if rank != 0:
         dist.destroy_process_group()
         return 0
