@@ -15,8 +15,7 @@ OUT = os.path.join(HERE, "libpobk.so")
 BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = [f"-DPOBK_K2_CPS={os.environ.get('POBK_K2_CPS', '1')}", f"-DPOBK_K2_NT={os.environ.get('POBK_K2_NT', '512')}",
-          f"-DPOBK_K2_EPT={os.environ.get('POBK_K2_EPT', '8')}", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
+COMMON = [f"-DPOBK_K2_MAXJ={os.environ.get('POBK_K2_MAXJ', '24')}", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
           "-I" + os.path.join(HERE, "..", "include")]
 
 SOURCES = [

@@ -1,28 +1,40 @@
-// K2: persistent tiled wavefront sweep, warp-specialised.
+// K2: persistent tiled wavefront sweep.
 //
-// The rows of A~ are split into T tiles (one CTA per SM, cooperative launch).  A schedule step
-// (a category of pairwise-orthogonal rows) restricted to one tile is a "task".  The
-// sequential semantics of a sweep (Alg 5 loop) only order rows that share a
-// column, so a tile's task k may run once every NEIGHBOUR tile (one sharing a column with it) has
-// finished its tasks < k: per-tile progress counters at gpu scope replace the grid-wide barrier
-// between categories.  Results are bitwise those of K1/K3 (same per-row contract, common.cuh).
+// The rows of A~ are split into T tiles (one 512-thread CTA per SM, cooperative launch).  A
+// schedule step (a category of pairwise-orthogonal rows) restricted to one tile is a
+// "task".  The sequential semantics of a sweep (Alg 5 loop) only order rows that
+// share a column.  Columns touched by one tile only are "private" (kept in that CTA's shared
+// memory for the whole solve); the others are "shared".  A row is "interior" if all its columns
+// are private, else "boundary".
+//   * Inside a tile, task k runs after task k-1 (one named barrier per task).
+//   * Across tiles, only shared columns carry dependencies.  Every row touching a shared column c
+//     reads the value written by the previous row touching c (in schedule order, wrapping to the
+//     previous sweep) and writes the value read by the next one: each written value has exactly
+//     ONE consumer.  So the writer stores the new x~_c straight into that consumer's MAILBOX slot
+//     (global memory, laid out like the consumer's slice so the consumer's polling loads are
+//     coalesced), and the consumer polls its slots until they no longer hold the sentinel (a
+//     signalling-NaN bit pattern no arithmetic produces), then re-arms them.  8-byte relaxed
+//     accesses are single-copy atomic, so no flags, counters or fences are on the critical path;
+//     slots are double-buffered by sweep parity and the per-sweep grid barrier orders a slot's
+//     re-arm before its next write.
+// Results are bitwise those of K1/K3 and of the oracle (the per-row contract of common.cuh).
 //
-//  * x~ columns touched by one tile only ("private") live in that CTA's shared memory for the
-//    whole solve; the rest ("shared") live in global memory and are accessed at L2 (ld/st .cg).
-//    Within a task, rows touching only private columns ("interior") run before the neighbour
-//    wait; rows touching a shared column ("boundary") run after it.
-//  * The tile's matrix data (val, col, row extents, f~, ||a~_i||^2) is a sequence of <= 40 KB
-//    chunks streamed by 1-D TMA (cp.async.bulk, L2 evict-first) into a 3-slot shared-memory ring,
-//    across task and sweep boundaries (A does not depend on x~).
-//  * Warp 31 is the CONTROL warp: it issues the TMA copies as slots free up, polls the neighbours'
-//    progress for the next boundary task and releases it to the compute warps, publishes the
-//    tile's progress when all compute warps finished a task (gpu-scope fence off the compute
-//    critical path), and runs the per-sweep stop decision.  Warps 0..30 COMPUTE: they flow
-//    through the chunks without CTA-wide barriers; one named barrier per task orders
-//    consecutive tasks inside the tile.
-//  * The RSE is accumulated by the LAST writer of every column in the sweep (the
-//    row of highest step touching it): no extra pass over x~; per-warp partials are reduced in a
-//    fixed order, tiles in tile order (deterministic).
+//  * Rows are stored as SLICES of <= 32 rows, one lane per row, in ELL order inside the slice
+//    (entry j of lane r at j*R + r; a task's rows are sorted by length before slicing so the
+//    padding is small; padding entries are value +0 on a private "zero slot" column): coalesced,
+//    conflict-free val/col loads, the row sum runs left to right in one thread (the oracle's
+//    order) and ||a~_i||^2 is recomputed in registers from the row (the oracle's left-to-right
+//    sum), so a row streams 12 B per stored entry + 10 B (f~, length), and a boundary row another
+//    4 B per entry (the mailbox slot its new value goes to).
+//  * A task's boundary slices come first; their warps load the private operands, then poll the
+//    mailboxes; the interior slices run meanwhile on the other warps.
+//  * The tile's slices are packed, across task boundaries, into <= 16 KB chunks streamed by 1-D
+//    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (warp 15),
+//    which never touches x~.
+//  * The RSE is evaluated at the end of each sweep by each tile over the columns
+//    it owns (its private ones in shared memory, and the shared ones whose last writer in the
+//    sweep it holds; that writer also stores the value to x~ in global memory).  Partials are
+//    combined in fixed orders; one grid-wide decision per sweep.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,50 +52,38 @@
 namespace pobk {
 
 namespace {
-#ifndef POBK_K2_CPS
-#define POBK_K2_CPS 1
+constexpr int kNT = 512;            // threads per CTA (one CTA per SM)
+constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
+constexpr int kNC = kNCW * 32;      // compute threads
+constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
+constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
+constexpr int kMinSlots = 4, kMaxSlots = 12;
+constexpr int kSliceRows = 32;      // rows per slice (one lane each)
+#ifndef POBK_K2_MAXJ
+#define POBK_K2_MAXJ 24
 #endif
-constexpr int kCPS = POBK_K2_CPS;   // CTAs (tiles) per SM
-#ifndef POBK_K2_NT
-#define POBK_K2_NT 1024
-#endif
-constexpr int kNT = POBK_K2_NT / kCPS;  // threads per CTA
-constexpr int kNCW = kNT / 32 - 1;  // compute warps (the last warp = control)
-constexpr int kSlots = 3;           // TMA ring depth
-constexpr int kChunkCap = 40 * 1024 / kCPS;
-#ifndef POBK_K2_EPT
-#define POBK_K2_EPT 4
-#endif
-constexpr int kEPT = POBK_K2_EPT;   // entries per compute thread per chunk (chunk nnz <= kEPT * compute threads)
-constexpr int kNbMax = 32;          // max neighbour tiles (one control-warp lane each)
-constexpr int kMaxChunks = 1024;    // max chunks per tile (metadata lives in shared memory)
-constexpr int kFlagStride = 32;     // ints between progress counters (one 128-B line each)
-constexpr int kSmemLimit = 228 * 1024 / kCPS - 1024;
-constexpr unsigned kShared = 0x80000000u, kLast = 0x40000000u, kIdx = 0x3FFFFFFFu;
-constexpr int kFirstBoundary = 1, kLastOfTask = 2;
+constexpr int kMaxJ = POBK_K2_MAXJ; // entries per row whose x~ is kept in registers between passes (<= 32)
+constexpr int kBatch = 8;           // loads issued together
+constexpr int kSmemTotal = 227 * 1024;
+constexpr int kMetaBudget = 16 * 1024;  // slice/chunk/task metadata in shared memory
+constexpr unsigned kShared = 0x80000000u, kIdx = 0x7FFFFFFFu;
+constexpr unsigned kWrap = 0x80000000u;  // mailbox target of a sweep's last writer: next sweep's slot
+constexpr unsigned long long kSentinel = 0x7FF0DEADBEEFCAFEull;  // signalling NaN: "slot empty"
+constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15LL); }
 
-// chunk block layout (bytes, each section 16-B aligned): val[nnz] f[rows] nrm2[rows] col[nnz] rp[rows+1]
-struct ChunkLayout {
-  int o_val, o_f, o_n, o_col, o_rp, bytes;
-  __host__ __device__ ChunkLayout(int rows, int nnz) {
-    o_val = 0;
-    o_f = a16(8LL * nnz);
-    o_n = o_f + a16(8LL * rows);
-    o_col = o_n + a16(8LL * rows);
-    o_rp = o_col + a16(4LL * nnz);
-    bytes = o_rp + a16(4LL * (rows + 1));
+// slice block (bytes): val[W*R] f[R] (fp64) | col[W*R] (u32: shared flag | index)
+//                      | [boundary slices] mout[W*R] (u32: wrap flag | mailbox index) | len[R] (u16)
+struct SliceLayout {
+  int o_f, o_col, o_mout, o_len, bytes;
+  __host__ __device__ SliceLayout(int R, int W, bool bnd) {
+    o_f = 8 * W * R;
+    o_col = o_f + 8 * R;
+    o_mout = o_col + 4 * W * R;
+    o_len = o_mout + (bnd ? 4 * W * R : 0);
+    bytes = a16(o_len + 2 * R);
   }
-};
-
-struct ChunkMeta {
-  int rows, nnz, task, flags;  // task = index in the tile's per-sweep task list
-  long long off;               // byte offset of the block in the stream
-};
-
-struct TaskMeta {
-  int step, k_next, boundary, pad;  // k_next >= nsteps: first task of the next sweep
 };
 
 struct SyncState {
@@ -97,34 +97,37 @@ struct SyncState {
 struct K2Args {
   const unsigned char* stream;
   const long long* tile_off;  // [T] byte offset of each tile's first chunk
-  const ChunkMeta* meta;
+  const int4* smeta;          // slices: {chunk | R << 20, offset in chunk, W, mailbox base (boundary)}
+  const int* tile_slice;      // [T+1]
+  const int4* cmeta;          // chunks: {offset from tile base, bytes, slices, 0}
   const int* tile_chunk;      // [T+1]
-  const TaskMeta* tmeta;
+  const int4* tmeta;          // tasks: {first slice, n_boundary | n_interior << 16, step, 0}
   const int* tile_task;       // [T+1]
-  const int* nbr;             // [T*kNbMax], -1 padded
   const int* pmap_ptr;        // [T+1]
   const int* pmap;            // private columns (global ids), tile by tile
-  double* xg;                 // x~ (RCM frame); authoritative for shared columns
+  const int* lastcol_ptr;     // [T+1]
+  const int* lastcol;         // shared columns whose last writer in a sweep is in the tile, tile by tile
+  unsigned long long* mbox;   // [2*NB] mailboxes (fp64 bits or kSentinel), parity-major
+  long long NB;
+  double* xg;                 // x~ (RCM frame): x0 in, final out; shared columns' sweep-final values
   const double* xst;          // x~*
-  int* progress;              // [T*kFlagStride]
   SyncState* sync;
   double* partials;           // [2*T]
   Ctrl* ctrl;
-  int nsteps, T;
-  int nck_max, ntask_max, np_max;  // shared-memory sizing
-  int debug;                       // development timing experiments (POBK_K2_DEBUG): 2 = no neighbour wait
-  unsigned long long* prof;        // optional [T*8] compute-warp phase clocks (POBK_K2_PROFILE=1)
+  int T, NS;
+  int nsl_max, nck_max, ntask_max, np_max;  // shared-memory sizing
+  unsigned long long* trace;  // optional [T*ntask_max*12] globaltimer stamps of one sweep (POBK_K2_TRACE=s)
+  int trace_sweep;
 };
 
 // shared-memory control block
 struct Ctl {
-  unsigned long long full[4];  // TMA completion mbarriers
-  int released[4];             // compute-warp releases per slot (cumulative)
-  int go;                      // task sequence numbers released to the compute warps
-  int done;                    // compute-warp task completions (cumulative)
-  int epoch;                   // sweeps decided
+  unsigned long long full[kMaxSlots];  // TMA completion mbarriers
+  int released[kMaxSlots];             // slices consumed per slot (cumulative)
+  unsigned long long issued;           // chunks issued (sequence number)
   int stop;
-  double part[32];             // per-compute-warp RSE partials
+  int pad;
+  double part[32];                     // per-compute-warp RSE partials
 };
 
 // ------------------------------------------------------------------ PTX helpers (TMA, mbarrier)
@@ -136,7 +139,7 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 // 1-D bulk copy global -> shared, completing on an mbarrier; the matrix stream is read once per
-// sweep and must not evict x~ from L2, so it carries an L2 evict-first policy.
+// sweep and must not evict x~ or the mailboxes from L2, so it carries an L2 evict-first policy.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* b,
                                             unsigned long long policy) {
   asm volatile(
@@ -157,342 +160,451 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
 __device__ __forceinline__ int ld_vol_shared(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ unsigned long long ld_vol_shared64(const unsigned long long* p) {
+  return *(const volatile unsigned long long*)p;
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-__global__ void __launch_bounds__(kNT, kCPS) k2_sweeps(K2Args a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;                                   // kSlots * kChunkCap
-  Ctl* ctl = (Ctl*)(smem + kSlots * kChunkCap);
-  int4* cmeta = (int4*)(ctl + 1);                               // [nck_max] {rows, nnz, task, flags}
-  int* coff = (int*)(cmeta + a.nck_max);                        // [nck_max] byte offset from the tile base
-  int4* tmeta = (int4*)(coff + ((a.nck_max + 3) & ~3));          // [ntask_max]
-  double* xloc = (double*)(tmeta + a.ntask_max);                // [np_max] private x~
-  double* xsloc = xloc + a.np_max;                              // [np_max] private x~* (RSE stop)
+// ------------------------------------------------------------------ slice arithmetic
+// All shared-memory operands are addressed through 32-bit shared-window addresses held in
+// registers ("opaque": the compiler may not rematerialise the window base inside predicated
+// code, which serialised the loads), and predicated PTX stores replace branches.
+__device__ __forceinline__ unsigned opaque(unsigned v) {
+  asm volatile("mov.u32 %0, %0;" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ double lds64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ unsigned lds32(unsigned a) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ unsigned lds16(unsigned a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64_if(unsigned p, unsigned a, double v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.shared.f64 [%1], %2;\n}" ::"r"(p), "r"(a), "d"(v)
+               : "memory");
+}
+// mailbox word: relaxed gpu-scope (single-copy atomic, observed at L2)
+__device__ __forceinline__ unsigned long long ldm_if(unsigned p, const unsigned long long* a, unsigned long long dflt) {
+  unsigned long long v = dflt;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.relaxed.gpu.global.b64 %0, [%2];\n}"
+               : "+l"(v)
+               : "r"(p), "l"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsigned long long v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a),
+               "l"(v)
+               : "memory");
+}
 
-  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, wl = tid & 31;
+// A slice in the ring (shared-window address blk): lane r < R holds row r.  Entries j >= len_r
+// of a row are ELL padding: value +0 and the private "zero slot" column (x~ = +0, never written),
+// so including them in the sums adds +0 * +0 = +0 and changes no bit (a row sum starting at +0
+// is never -0); only the stores are predicated on j < len_r.  Rows are applied with the per-row
+// contract of common.cuh (Eq 1.2).
+struct SliceAddr {
+  unsigned vb, cb, mb;  // this lane's val / col / mout entry 0; entry j at + j*R*8 / + j*R*4
+  unsigned vs, cs;      // strides
+  int myl;              // row length (0 for lanes >= R)
+  double f;             // f~_i
+  __device__ __forceinline__ SliceAddr(unsigned blk, int R, int W, bool bnd, int lane) {
+    const int ln = lane < R ? lane : 0;
+    vs = 8u * R;
+    cs = 4u * R;
+    const SliceLayout L(R, W, bnd);
+    vb = opaque(blk + 8u * ln);
+    cb = opaque(blk + (unsigned)L.o_col + 4u * ln);
+    mb = blk + (unsigned)L.o_mout + 4u * ln;
+    f = lds64(blk + (unsigned)L.o_f + 8u * ln);
+    myl = lane < R ? (int)lds16(blk + (unsigned)L.o_len + 2u * ln) : 0;
+  }
+};
+
+// interior slice: every column private (shared memory at xb); pass 2 re-reads x~ from shared
+// memory (unchanged in between: no other row of the category touches these columns)
+__device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsigned xb) {
+  double s = 0.0, n2 = 0.0;
+  for (int jb = 0; jb < W; jb += kBatch) {
+    unsigned c[kBatch];
+    double av[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+#pragma unroll
+    for (int u = 0; u < kBatch; u++)
+      if (jb + u < W) {
+        s = __dadd_rn(s, __dmul_rn(av[u], xv[u]));
+        n2 = __dadd_rn(n2, __dmul_rn(av[u], av[u]));
+      }
+  }
+  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+  for (int jb = 0; jb < W; jb += kBatch) {
+    unsigned c[kBatch];
+    double av[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) {
+      c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+      av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
+  }
+}
+
+// boundary slice, in two halves: pre() loads the PRIVATE x~ (final for this step as soon as the
+// tile's previous task is done) and notes the shared entries; post() polls the shared entries'
+// mailboxes (this lane's slot of entry j: mbox_in + j*R), re-arms them, applies the rows, writes
+// private results to shared memory and shared results to their consumers' mailboxes (and, for a
+// sweep's last writer, to x~ in global memory).
+struct BSlice {
+  double xr[kMaxJ];
+  unsigned shm;  // bit j: entry j (< kMaxJ) is a shared column of this lane's row
+  __device__ __forceinline__ void pre(const SliceAddr& S, int W, unsigned xb) {
+    shm = 0u;
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+      if (jb < W) {
+        unsigned c[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const bool sh = (c[u] & kShared) && jb + u < S.myl;
+          shm |= sh ? (1u << (jb + u)) : 0u;
+          xr[jb + u] = (c[u] & kShared) ? 0.0 : lds64(xb + 8u * c[u]);
+        }
+      }
+    }
+  }
+  // poll this lane's shared entries j < kMaxJ until every lane of the warp has all of them
+  __device__ __forceinline__ void poll(const SliceAddr& S, int W, int R, unsigned long long* mbox_in) {
+    unsigned pend = shm;
+    while (true) {
+#pragma unroll
+      for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+        if (jb < W) {
+#pragma unroll
+          for (int u = 0; u < kBatch; u++) {
+            const unsigned long long w =
+                ldm_if((pend >> (jb + u)) & 1u, mbox_in + (size_t)(jb + u) * R, (unsigned long long)__double_as_longlong(xr[jb + u]));
+            xr[jb + u] = __longlong_as_double((long long)w);
+          }
+        }
+      }
+      unsigned np = 0u;
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j++)
+        if ((pend >> j) & 1u) np |= ((unsigned long long)__double_as_longlong(xr[j]) == kSentinel) ? (1u << j) : 0u;
+      pend = np;
+      if (!__any_sync(kFull, pend != 0u)) break;
+    }
+    // re-arm the consumed slots for the sweep after next (ordered by the per-sweep grid barrier)
+#pragma unroll
+    for (int j = 0; j < kMaxJ; j++) stm_if((shm >> j) & 1u, mbox_in + (size_t)j * R, kSentinel);
+  }
+  __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, double* xg, unsigned long long* mbox_in,
+                                       unsigned long long* mbox_p, unsigned long long* mbox_q, int R) {
+    double s = 0.0, n2 = 0.0;
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+      if (jb < W) {
+#pragma unroll
+        for (int u = 0; u < kBatch; u++)
+          if (jb + u < W) {
+            const double a = lds64(S.vb + (jb + u) * S.vs);
+            s = __dadd_rn(s, __dmul_rn(a, xr[jb + u]));
+            n2 = __dadd_rn(n2, __dmul_rn(a, a));
+          }
+      }
+    }
+    for (int j = kMaxJ; j < W; j++) {
+      const unsigned cj = lds32(S.cb + j * S.cs);
+      const double a = lds64(S.vb + j * S.vs);
+      double x = 0.0;
+      if ((cj & kShared) && j < S.myl) {
+        unsigned long long w;
+        do {
+          w = ldm_if(1u, mbox_in + (size_t)j * R, 0ull);
+        } while (w == kSentinel);  // (re-armed in pass 2, after it is read again)
+        x = __longlong_as_double((long long)w);
+      } else if (!(cj & kShared)) {
+        x = lds64(xb + 8u * (cj & kIdx));
+      }
+      s = __dadd_rn(s, __dmul_rn(a, x));
+      n2 = __dadd_rn(n2, __dmul_rn(a, a));
+    }
+    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+      if (jb < W) {
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const int j = jb + u;
+          const unsigned jj = (unsigned)min(j, W - 1);
+          const unsigned c = lds32(S.cb + jj * S.cs);
+          const double x1 = __dadd_rn(xr[j], __dmul_rn(alpha, lds64(S.vb + jj * S.vs)));
+          const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
+          sts64_if(act & (sh ^ 1u), xb + 8u * (c & kIdx), x1);
+          const unsigned mo = lds32(S.mb + jj * S.cs);
+          const unsigned long long bits = (unsigned long long)__double_as_longlong(x1);
+          stm_if(act & sh, ((mo & kWrap) ? mbox_q : mbox_p) + (mo & ~kWrap), bits);
+          if (act & sh & (mo >> 31)) st_cg(xg + (c & kIdx), x1);  // the sweep's last writer of c
+        }
+      }
+    }
+    for (int j = kMaxJ; j < W; j++) {  // tail: the slot still holds the consumed value (re-armed now)
+      const unsigned cj = lds32(S.cb + j * S.cs), idx = cj & kIdx;
+      const double a = lds64(S.vb + j * S.vs);
+      if ((cj & kShared) && j < S.myl) {
+        const unsigned long long w = ldm_if(1u, mbox_in + (size_t)j * R, 0ull);
+        stm_if(1u, mbox_in + (size_t)j * R, kSentinel);
+        {
+          const double x1 = __dadd_rn(__longlong_as_double((long long)w), __dmul_rn(alpha, a));
+          const unsigned mo = lds32(S.mb + j * S.cs);
+          stm_if(1u, ((mo & kWrap) ? mbox_q : mbox_p) + (mo & ~kWrap), (unsigned long long)__double_as_longlong(x1));
+          if (mo & kWrap) st_cg(xg + idx, x1);
+        }
+      } else if (!(cj & kShared) && j < S.myl) {
+        const unsigned ca = xb + 8u * idx;
+        sts64_if(1u, ca, __dadd_rn(lds64(ca), __dmul_rn(alpha, a)));
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int NS = a.NS;
+  unsigned char* ring = smem;                                // NS * kSlot
+  Ctl* ctl = (Ctl*)(smem + NS * kSlot);
+  int4* smeta = (int4*)(ctl + 1);                            // [nsl_max]
+  int4* cmeta = smeta + a.nsl_max;                           // [nck_max]
+  int4* tmeta = cmeta + a.nck_max;                           // [ntask_max]
+  double* xloc = (double*)(tmeta + a.ntask_max);             // [np_max + 1] private x~ + the zero slot
+  double* xsloc = xloc + a.np_max + 1;                       // [np_max] private x~* (RSE stop)
+
+  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int s0 = a.tile_slice[t], nsl = a.tile_slice[t + 1] - s0;
   const int c0 = a.tile_chunk[t], nck = a.tile_chunk[t + 1] - c0;
   const int j0 = a.tile_task[t], ntask = a.tile_task[t + 1] - j0;
   const int q0 = a.pmap_ptr[t], np = a.pmap_ptr[t + 1] - q0;
-  const int nsteps = a.nsteps;
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
+  const bool rse = mode == POBK_STOP_RSE;
 
   if (tid == 0) {
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < kMaxSlots; i++) {
       mbar_init(&ctl->full[i], 1);
       ctl->released[i] = 0;
     }
-    ctl->go = 0;
-    ctl->done = 0;
-    ctl->epoch = 0;
+    ctl->issued = 0;
     ctl->stop = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = tid; j < nck; j += kNT) {
-    const ChunkMeta mt = a.meta[c0 + j];
-    cmeta[j] = make_int4(mt.rows, mt.nnz, mt.task, mt.flags);
-    coff[j] = (int)(mt.off - a.tile_off[t]);
-  }
-  for (int j = tid; j < ntask; j += kNT) {
-    const TaskMeta tm = a.tmeta[j0 + j];
-    tmeta[j] = make_int4(tm.step, tm.k_next, tm.boundary, 0);
-  }
+  for (int j = tid; j < nsl; j += kNT) smeta[j] = a.smeta[s0 + j];
+  for (int j = tid; j < nck; j += kNT) cmeta[j] = a.cmeta[c0 + j];
+  for (int j = tid; j < ntask; j += kNT) tmeta[j] = a.tmeta[j0 + j];
+  if (tid == 0) xloc[a.np_max] = 0.0;  // the zero slot of the ELL padding (never written)
   for (int j = tid; j < np; j += kNT) {
-    const int gcol = a.pmap[q0 + j];
-    xloc[j] = a.xg[gcol];
-    xsloc[j] = (mode == POBK_STOP_RSE) ? a.xst[gcol] : 0.0;
+    const int gcol = a.pmap[q0 + j];  // -1: a hole of the bank-aware placement
+    xloc[j] = gcol >= 0 ? a.xg[gcol] : 0.0;
+    xsloc[j] = (rse && gcol >= 0) ? a.xst[gcol] : 0.0;
   }
   __syncthreads();
 
   if (warp == kNCW) {
-    // ================================================================ control warp
-    const unsigned long long pol = policy_evict_first();
-    const int my_nb = wl < kNbMax ? a.nbr[t * kNbMax + wl] : -1;
-    const unsigned char* tbase = a.stream + a.tile_off[t];
-    long long g_issue = 0;   // next chunk sequence to issue
-    long long j_go = 0;      // next task sequence to release
-    long long j_pub = 0;     // next task sequence to publish
-    long long sweep = 0;     // sweeps completed (decided)
-    bool finished = (maxs <= 0);
-    while (!finished) {
-      // (1) TMA: keep the ring full (a slot is free once all compute warps released its last use);
-      //     never more than one sweep ahead of the decided sweep
-      if (nck > 0) {
-        while (g_issue < (sweep + 2) * (long long)nck) {
-          const int slot = (int)(g_issue % kSlots);
-          const long long use = g_issue / kSlots;
-          if (use > 0 && ld_vol_shared(&ctl->released[slot]) < (int)(use * kNCW)) break;
-          if (wl == 0) {
-            const int c = (int)(g_issue % nck);
-            const int4 mt = cmeta[c];
-            const int bytes = ChunkLayout(mt.x, mt.y).bytes;
-            mbar_expect_tx(&ctl->full[slot], bytes);
-            tma_load_1d(ring + slot * kChunkCap, tbase + coff[c], bytes, &ctl->full[slot], pol);
-          }
-          __syncwarp();
-          g_issue++;
+    // ================================================================ producer warp (TMA only)
+    if (lane == 0 && nck > 0 && maxs > 0) {
+      const unsigned long long pol = policy_evict_first();
+      const unsigned char* tbase = a.stream + a.tile_off[t];
+      int cum[kMaxSlots];
+      for (int i = 0; i < kMaxSlots; i++) cum[i] = 0;
+      const unsigned long long gmax = (unsigned long long)maxs * (unsigned long long)nck;
+      unsigned long long g = 0;
+      int slot = 0, c = 0;
+      while (!ld_vol_shared(&ctl->stop)) {
+        if (g >= gmax || (g >= (unsigned long long)NS && ld_vol_shared(&ctl->released[slot]) < cum[slot])) {
+          __nanosleep(64);
+          continue;
         }
+        const int4 cm = cmeta[c];
+        mbar_expect_tx(&ctl->full[slot], (unsigned)cm.y);
+        tma_load_1d(ring + slot * kSlot, tbase + cm.x, (unsigned)cm.y, &ctl->full[slot], pol);
+        cum[slot] += cm.z;
+        g++;
+        if (++slot == NS) slot = 0;
+        if (++c == nck) c = 0;
+        *(volatile unsigned long long*)&ctl->issued = g;
       }
-      // (2) release the next task of this sweep once its neighbours are far enough
-      if (ntask > 0 && j_go < (sweep + 1) * (long long)ntask) {
-        const int4 tm = tmeta[(int)(j_go % ntask)];
-        const long long sw = j_go / ntask;
-        bool ok = true;
-        if (tm.z && !(a.debug & 2)) {
-          const int need = (int)(sw * nsteps + tm.x);
-          const int v = my_nb >= 0 ? ld_relaxed(a.progress + my_nb * kFlagStride) : need;
-          ok = __all_sync(0xffffffffu, v >= need);
-        }
-        if (ok) {
-          if (tm.z) __threadfence();  // acquire the neighbours' writes at gpu scope ...
-          j_go++;
-          if (wl == 0) *(volatile int*)&ctl->go = (int)j_go;  // ... and hand them to the CTA
-          __syncwarp();
-        }
-      }
-      // (3) publish finished tasks (all compute warps reported the task)
-      if (ntask > 0 && j_pub < j_go && ld_vol_shared(&ctl->done) >= (int)((j_pub + 1) * kNCW)) {
-        const int4 tm = tmeta[(int)(j_pub % ntask)];
-        const long long sw = j_pub / ntask;
-        __threadfence();
-        if (wl == 0)
-          asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(a.progress + t * kFlagStride),
-                       "r"((int)(sw * nsteps + tm.y))
-                       : "memory");
-        __syncwarp();
-        j_pub++;
-      }
-      // (4) end of sweep: every task of the sweep published (or no tasks)
-      if ((ntask == 0) || (j_pub >= (sweep + 1) * (long long)ntask)) {
-        const long long s1 = sweep + 1;
-        const bool due = mode != POBK_STOP_NONE && ((s1 % every) == 0 || s1 >= maxs);
-        int stop = 0;
-        if (due) {
-          if (wl == 0) {
-            double part = 0.0;
-            if (ntask > 0)
-              for (int w = 0; w < kNCW; w++) part += ((volatile double*)ctl->part)[w];
-            const int par = (int)(s1 & 1);
-            a.partials[par * a.T + t] = part;
-            __threadfence();
-            const unsigned old = atomicAdd(&a.sync->arrive[par], 1u);
-            if (old == (unsigned)a.T - 1) {
-              __threadfence();
-              double tot = 0.0;
-              for (int b = 0; b < a.T; b++) tot += ld_cg(a.partials + par * a.T + b);
-              const double v = sqrt(tot) / sqrt(a.ctrl->den);
-              int st = 0, term = POBK_TERM_MAX_SWEEPS;
-              if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
-              else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
-              else if (s1 >= maxs) st = 1;
-              a.sync->arrive[par] = 0;
-              a.sync->stop = st;
-              a.ctrl->value = v;
-              a.ctrl->sweeps = s1;
-              a.ctrl->term = term;
-              __threadfence();
-              st_release(&a.sync->epoch, (int)s1);
-            } else {
-              while (ld_relaxed(&a.sync->epoch) < (int)s1) {
-              }
-              __threadfence();
-            }
-            stop = ld_relaxed(&a.sync->stop);
-          }
-          stop = __shfl_sync(0xffffffffu, stop, 0);
-        } else if (s1 >= maxs) {
-          stop = 1;
-          if (t == 0 && wl == 0) {
-            a.ctrl->sweeps = s1;
-            a.ctrl->term = POBK_TERM_MAX_SWEEPS;
-          }
-        }
-        sweep = s1;
-        if (wl == 0) {
-          *(volatile int*)&ctl->stop = stop;
-          __threadfence_block();
-          *(volatile int*)&ctl->epoch = (int)sweep;
-        }
-        __syncwarp();
-        if (stop) finished = true;
-      }
-    }
-    // drain the TMA copies issued beyond the consumed ones
-    if (wl == 0 && nck > 0) {
-      const long long consumed = sweep * nck;
-      for (long long h = consumed; h < g_issue; h++)
-        mbar_wait(&ctl->full[(int)(h % kSlots)], (unsigned)((h / kSlots) & 1));
+      // drain: every issued copy must land before the CTA exits
+      const unsigned long long h0 = g > (unsigned long long)NS ? g - NS : 0;
+      for (unsigned long long h = h0; h < g; h++)
+        mbar_wait(&ctl->full[(int)(h % (unsigned)NS)], (unsigned)((h / (unsigned)NS) & 1));
     }
   } else {
     // ================================================================ compute warps
-    // Entry-parallel, three phases per chunk (the oracle's arithmetic, common.cuh):
-    //   A  every thread takes entries p = cid + e*NC: gathers x~ (smem or L2) and forms
-    //      a_p * x_p, written in place over val[p] in the ring slot (val kept in registers)
-    //   B  one thread per row sums its products left to right, alpha = (f - s) / nrm2, and
-    //      broadcasts alpha over the row's entry slots
-    //   C  every thread scatters x_p + alpha * a_p for its entries (smem or L2), and the last
-    //      writer of a column adds (x - x*)^2 to the RSE partial
-    constexpr int NC = kNCW * 32;
-    const int cid = tid;
-    double acc_rse = 0.0;
-    long long sweep = 0, g = 0;
-    unsigned long long pf_go = 0, pf_full = 0, pf_bar = 0, pf_epoch = 0;
-    unsigned long long pf_a = 0, pf_ab = 0, pf_b = 0, pf_bb = 0, pf_c = 0;
-    const unsigned long long pf_t0 = clock64();
+    const unsigned xb = opaque(smem_u32(xloc));
+    const unsigned ring_s = opaque(smem_u32(ring));
+    long long sweep = 0;
     while (sweep < maxs) {
-      acc_rse = 0.0;
-      for (int i = 0; i < nck; i++, g++) {
-        const int4 mt = cmeta[i];
-        const int rows = mt.x, nnz = mt.y, flags = mt.w;
-        unsigned long long pc0 = clock64();
-        if (flags & kFirstBoundary) {
-          const int jtask = (int)(sweep * ntask + mt.z);
-          while (ld_vol_shared(&ctl->go) <= jtask) {
+      unsigned long long* const mbox_p = a.mbox + (size_t)(sweep & 1) * a.NB;        // this sweep's slots
+      unsigned long long* const mbox_q = a.mbox + (size_t)((sweep + 1) & 1) * a.NB;  // the next sweep's
+      const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
+      for (int ti = 0; ti < ntask; ti++) {
+        const int4 tm = tmeta[ti];
+        const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
+        unsigned long long* trp = tr ? a.trace + ((size_t)t * a.ntask_max + ti) * 12 : nullptr;
+        if (tr && warp == 0 && lane == 0) trp[0] = gtimer();
+        for (int q = warp; q < ntot; q += kNCW) {
+          const bool bnd = q < nbnd;
+          const int4 sl = smeta[tm.x + q];
+          const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
+          const unsigned long long g = (unsigned long long)sweep * nck + chunk;
+          const int slot = (int)(g % (unsigned)NS);
+          while (ld_vol_shared64(&ctl->issued) <= g) {
           }
-          __threadfence_block();
-        }
-        unsigned long long pc1 = clock64();
-        const int slot = (int)(g % kSlots);
-        mbar_wait(&ctl->full[slot], (unsigned)((g / kSlots) & 1));
-        unsigned long long pc2 = clock64();
-        pf_go += pc1 - pc0;
-        pf_full += pc2 - pc1;
-        unsigned char* blk = ring + slot * kChunkCap;
-        const ChunkLayout L(rows, nnz);
-        double* val = (double*)(blk + L.o_val);
-        const double* fv = (const double*)(blk + L.o_f);
-        const double* nv = (const double*)(blk + L.o_n);
-        const unsigned* col = (const unsigned*)(blk + L.o_col);
-        const int* rp = (const int*)(blk + L.o_rp);
-        unsigned cc[kEPT];
-        double av[kEPT], xv[kEPT], sv[kEPT];
-        // ---- A: gather and products
-#pragma unroll
-        for (int e = 0; e < kEPT; e++) {
-          const int p = cid + e * NC;
-          cc[e] = 0u;
-          av[e] = 0.0;
-          xv[e] = 0.0;
-          sv[e] = 0.0;
-          if (p < nnz) {
-            cc[e] = col[p];
-            av[e] = val[p];
+          mbar_wait(&ctl->full[slot], (unsigned)((g / (unsigned)NS) & 1));
+          const unsigned blk = ring_s + (unsigned)(slot * kSlot + sl.y);
+          if (tr && lane == 0 && (q == 0 || q == nbnd)) trp[q == 0 ? 4 : 6] = gtimer();
+          const SliceAddr S(blk, R, W, bnd, lane);
+          if (bnd) {
+            BSlice B;
+            B.pre(S, W, xb);
+            if (tr && q == 0 && lane == 0) trp[8] = gtimer();
+            unsigned long long* const mbox_in = mbox_p + sl.w + (lane < R ? lane : 0);
+            B.poll(S, W, R, mbox_in);
+            if (tr && q == 0 && lane == 0) trp[1] = gtimer();
+            B.post(S, W, xb, a.xg, mbox_in, mbox_p, mbox_q, R);
+          } else {
+            slice_interior(S, W, xb);
           }
+          __syncwarp();
+          if (lane == 0) atomicAdd(&ctl->released[slot], 1);
+          if (tr && lane == 0 && (q == 0 || q == nbnd)) trp[q == 0 ? 5 : 7] = gtimer();
         }
-#pragma unroll
-        for (int e = 0; e < kEPT; e++) {
-          const int p = cid + e * NC;
-          if (p < nnz) {
-            const unsigned c = cc[e], idx = c & kIdx;
-            if (c & kShared) {
-              xv[e] = ld_cg(a.xg + idx);
-              if (c & kLast) sv[e] = __ldg(a.xst + idx);
-            } else {
-              xv[e] = xloc[idx];
-              if (c & kLast) sv[e] = xsloc[idx];
-            }
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < kEPT; e++) {
-          const int p = cid + e * NC;
-          if (p < nnz) val[p] = __dmul_rn(av[e], xv[e]);
-        }
-        unsigned long long pA = clock64();
-        named_bar(1, NC);
-        unsigned long long pA2 = clock64();
-        // ---- B: per-row sums (left to right), alpha, broadcast
-        for (int r = cid; r < rows; r += NC) {
-          const int p0 = rp[r], p1 = rp[r + 1];
-          double sum = 0.0;
-          int p = p0;
-          for (; p + 8 <= p1; p += 8) {  // batch the loads, keep the left-to-right additions
-            double v[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++) v[j] = val[p + j];
-#pragma unroll
-            for (int j = 0; j < 8; j++) sum = __dadd_rn(sum, v[j]);
-          }
-          for (; p < p1; p++) sum = __dadd_rn(sum, val[p]);
-          const double alpha = __ddiv_rn(__dsub_rn(fv[r], sum), nv[r]);
-          for (p = p0; p < p1; p++) val[p] = alpha;
-        }
-        unsigned long long pB = clock64();
-        named_bar(1, NC);
-        unsigned long long pB2 = clock64();
-        // ---- C: scatter
-#pragma unroll
-        for (int e = 0; e < kEPT; e++) {
-          const int p = cid + e * NC;
-          if (p < nnz) {
-            const unsigned c = cc[e], idx = c & kIdx;
-            const double xn = __dadd_rn(xv[e], __dmul_rn(val[p], av[e]));
-            if (c & kShared) st_cg(a.xg + idx, xn);
-            else xloc[idx] = xn;
-            if (c & kLast) {
-              const double d = xn - sv[e];
-              acc_rse = fma(d, d, acc_rse);
-            }
-          }
-        }
-        unsigned long long pC = clock64();
-        pf_a += pA - pc2; pf_ab += pA2 - pA; pf_b += pB - pA2; pf_bb += pB2 - pB; pf_c += pC - pB2;
-        if ((flags & kLastOfTask) && i == nck - 1 && mode == POBK_STOP_RSE) {
-          // this warp's RSE partial (fixed lane order) before it reports the sweep's last task
-          double w = acc_rse;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-          if (wl == 0) ctl->part[warp] = w;
-        }
-        // generic-proxy writes to the slot (products, alphas) before the next TMA refill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (wl == 0) {
-          __threadfence_block();
-          atomicAdd(&ctl->released[slot], 1);
-          if (flags & kLastOfTask) atomicAdd(&ctl->done, 1);
-        }
-        if (flags & kLastOfTask) {
-          const unsigned long long pb = clock64();
-          named_bar(1, NC);  // task k before task k+1 inside the tile
-          pf_bar += clock64() - pb;
-        }
+        named_bar(1, kNC);  // task k before task k+1 inside the tile
+        if (tr && warp == 0 && lane == 0) trp[3] = gtimer();
       }
       sweep++;
-      const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
+      // ---- end of sweep: a grid barrier every sweep (it also orders the mailbox re-arms of this
+      //      sweep before the writes of the next ones); the stop test when due
+      const bool due = mode == POBK_STOP_RSE && ((sweep % every) == 0 || sweep >= maxs);
       if (due) {
-        const unsigned long long pe = clock64();
-        while (ld_vol_shared(&ctl->epoch) < (int)sweep) {
+        // columns final for this sweep once the tile's last task is done: the private ones, and
+        // the shared ones whose last writer (row of the highest step) is in this tile
+        double acc = 0.0;
+        for (int j = tid; j < np; j += kNC) {
+          const double d = xloc[j] - xsloc[j];
+          acc = fma(d, d, acc);
         }
-        __threadfence_block();
-        pf_epoch += clock64() - pe;
-        if (ld_vol_shared(&ctl->stop)) break;
+        for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNC) {
+          const int c = a.lastcol[j];
+          const double d = ld_cg(a.xg + c) - __ldg(a.xst + c);
+          acc = fma(d, d, acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // fixed lane order
+        if (lane == 0) ctl->part[warp] = acc;
       }
-    }
-    if (a.prof && tid == 0) {
-      unsigned long long* o = a.prof + t * 16;
-      o[0] = pf_go; o[1] = pf_full; o[2] = pf_bar; o[3] = pf_epoch; o[4] = clock64() - pf_t0; o[5] = nck;
-      o[6] = pf_a; o[7] = pf_ab; o[8] = pf_b; o[9] = pf_bb; o[10] = pf_c;
+      named_bar(1, kNC);
+      if (warp == kPub) {
+        const int par = (int)(sweep & 1);
+        int last = 0;
+        if (lane == 0) {
+          double part = 0.0;
+          if (due)
+            for (int w2 = 0; w2 < kNCW; w2++) part += ((volatile double*)ctl->part)[w2];
+          a.partials[par * a.T + t] = part;
+          __threadfence();
+          last = atomicAdd(&a.sync->arrive[par], 1u) == (unsigned)a.T - 1;
+        }
+        last = __shfl_sync(kFull, last, 0);
+        if (last) {
+          __threadfence();
+          int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
+          double v = 0.0;
+          if (due) {
+            double tot = 0.0;  // tiles in tile order
+            for (int b0 = 0; b0 < a.T; b0 += 32) {
+              const double pv = b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
+              for (int j = 0; j < 32 && b0 + j < a.T; j++) tot += __shfl_sync(kFull, pv, j);
+            }
+            v = sqrt(tot) / sqrt(a.ctrl->den);
+            if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
+            else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
+          }
+          if (lane == 0) {
+            a.sync->arrive[par] = 0;
+            a.sync->stop = st;
+            if (due) a.ctrl->value = v;
+            a.ctrl->sweeps = sweep;
+            a.ctrl->term = term;
+            st_release(&a.sync->epoch, (int)sweep);
+          }
+        } else if (lane == 0) {
+          while (ld_acquire(&a.sync->epoch) < (int)sweep) {
+          }
+        }
+        int stop = 0;
+        if (lane == 0) stop = ld_relaxed(&a.sync->stop);
+        stop = __shfl_sync(kFull, stop, 0);
+        if (lane == 0) *(volatile int*)&ctl->stop = stop;
+      }
+      named_bar(2, kNC);
+      if (ld_vol_shared(&ctl->stop)) break;
     }
   }
   __syncthreads();
-  for (int j = tid; j < np; j += kNT) a.xg[a.pmap[q0 + j]] = xloc[j];
-}
-
-__global__ void k2_reset(int T, const int* k_first, int* progress, SyncState* sync) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x)
-    progress[t * kFlagStride] = k_first[t];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sync->arrive[0] = sync->arrive[1] = 0;
-    sync->epoch = 0;
-    sync->stop = 0;
+  for (int j = tid; j < np; j += kNT) {
+    const int gcol = a.pmap[q0 + j];
+    if (gcol >= 0) a.xg[gcol] = xloc[j];
   }
 }
 
-// f (user frame) into the f~ slots of the chunk stream
+__global__ void k2_reset(SyncState* sync) {
+  sync->arrive[0] = sync->arrive[1] = 0;
+  sync->epoch = 0;
+  sync->stop = 0;
+}
+
+// every mailbox slot empty, then each shared column's first reader of sweep 0 gets x~0
+__global__ void k2_mbox_fill(unsigned long long* mbox, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    mbox[i] = kSentinel;
+}
+__global__ void k2_mbox_seed(unsigned long long* mbox, int n, const int* __restrict__ idx, const int* __restrict__ col,
+                             const double* __restrict__ xt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v = xt[col[i]];
+    if (v != v) v = __longlong_as_double(0x7FF8000000000000ll);  // a NaN x0 never reads as the sentinel
+    mbox[idx[i]] = (unsigned long long)__double_as_longlong(v);
+  }
+}
+
+// f (user frame) into the f~ slots of the slice stream
 __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const int64_t* __restrict__ fslot,
                              const double* __restrict__ f, double* __restrict__ stream_d) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x)
@@ -501,27 +613,30 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 }  // namespace
 
 struct K2Plan {
-  int T = 0;
+  int T = 0, NS = 0;
   size_t smem = 0;
-  int nck_max = 1, ntask_max = 1, np_max = 1;
+  int nsl_max = 1, nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
   long long* tile_off = nullptr;
-  unsigned long long* prof = nullptr;
-  ChunkMeta* meta = nullptr;
-  TaskMeta* tmeta = nullptr;
-  int *tile_chunk = nullptr, *tile_task = nullptr, *nbr = nullptr, *pmap_ptr = nullptr, *pmap = nullptr;
-  int* k_first = nullptr;
-  int* progress = nullptr;
+  unsigned long long* trace = nullptr;
+  int4 *smeta = nullptr, *cmeta = nullptr, *tmeta = nullptr;
+  int *tile_slice = nullptr, *tile_chunk = nullptr, *tile_task = nullptr, *pmap_ptr = nullptr, *pmap = nullptr,
+      *lastcol_ptr = nullptr, *lastcol = nullptr, *seed_idx = nullptr, *seed_col = nullptr;
+  unsigned long long* mbox = nullptr;
+  long long NB = 0;
+  int nseed = 0;
   SyncState* sync = nullptr;
   double* partials = nullptr;
-  int32_t* orig_q = nullptr;   // tile-order row -> user-frame row
-  int64_t* fslot = nullptr;    // tile-order row -> double index of its f~ slot in the stream
+  int32_t* orig_q = nullptr;   // stream-order row -> user-frame row
+  int64_t* fslot = nullptr;    // stream-order row -> double index of its f~ slot in the stream
   std::vector<void*> allocs;
   // stats (bench)
   double private_frac = 0.0;   // fraction of nnz whose column is private
   double interior_frac = 0.0;  // fraction of rows that are interior
   long long stream_bytes = 0;
+  long long pad_entries = 0;   // ELL padding entries in the stream
   int nchunks = 0;
+  int ntask_total = 0;
 };
 
 namespace {
@@ -628,7 +743,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, p.device) == cudaSuccess) sms = prop.multiProcessorCount;
   const int64_t m = p.m;
-  int T = sms * kCPS;
+  int T = sms;
   if (tile_rows > 0) T = (int)std::max<int64_t>(1, std::min<int64_t>(T, (m + tile_rows - 1) / tile_rows));
   T = (int)std::min<int64_t>(T, std::max<int64_t>(1, p.nnz / 4096));
   // tiling: among T' in {T, T-4, T-8} (one tile per SM, a few SMs may idle) and the factorisations
@@ -659,24 +774,21 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   for (int k = 0; k < p.nsteps; k++)
     for (int q = p.sched.step_ptr[k]; q < p.sched.step_ptr[k + 1]; q++) step_of[p.sched.rows[q]] = k;
 
-  // columns: private / shared, last writer (row of the highest step touching the column)
-  std::vector<int32_t> col_tile(m, -1), last_row(m, -1);
+  // columns: owner tile / shared; a column no row touches stays constant and is kept private to
+  // tile 0 (it still counts in the RSE)
+  std::vector<int32_t> col_tile(m, -1);
   std::vector<uint8_t> shared(m, 0);
   for (int64_t i = 0; i < m; i++)
     for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) {
       const int32_t c = At.col[q];
       if (col_tile[c] < 0) col_tile[c] = tile[i];
       else if (col_tile[c] != tile[i]) shared[c] = 1;
-      if (last_row[c] < 0 || step_of[i] > step_of[last_row[c]]) last_row[c] = (int32_t)i;
     }
-  // private columns per tile (ascending), capped by shared memory
-  const size_t fixed = (size_t)kSlots * kChunkCap + sizeof(Ctl) + 256;
-  const size_t meta_bytes = (size_t)20 * kMaxChunks + 16 * (size_t)p.nsteps;
-  if (fixed + meta_bytes + 16 * 1024 > (size_t)kSmemLimit - 1024) {
-    why = "too many schedule steps for K2's shared memory";
-    return false;
-  }
-  const int np_cap = (int)((kSmemLimit - 1024 - fixed - meta_bytes) / 16);  // x~ and x~* per column
+  for (int64_t c = 0; c < m; c++)
+    if (col_tile[c] < 0) col_tile[c] = 0;
+  // private columns per tile (ascending), capped so that kMinSlots ring slots still fit
+  const size_t fixed = sizeof(Ctl) + 128;
+  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / 16 / 1.04) - 48;  // x~, x~*, zero slot, bank slack
   std::vector<int32_t> local(m, -1);
   std::vector<int> pmap_ptr(T + 1, 0);
   std::vector<int> pmap;
@@ -684,7 +796,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   {
     std::vector<std::vector<int32_t>> per(T);
     for (int64_t c = 0; c < m; c++)
-      if (!shared[c] && col_tile[c] >= 0) per[col_tile[c]].push_back((int32_t)c);
+      if (!shared[c]) per[col_tile[c]].push_back((int32_t)c);
     for (int t = 0; t < T; t++) {
       if ((int)per[t].size() > np_cap) {
         for (size_t j = np_cap; j < per[t].size(); j++) shared[per[t][j]] = 1;  // demote the overflow
@@ -695,185 +807,304 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       np_t[t] = (int)per[t].size();
     }
   }
-  // neighbours: tiles sharing a column
-  std::vector<std::set<int>> nbs(T);
-  {
-    std::vector<int64_t> cptr(m + 1, 0);
-    for (int64_t q = 0; q < At.nnz(); q++) cptr[At.col[q] + 1]++;
-    for (int64_t c = 0; c < m; c++) cptr[c + 1] += cptr[c];
-    std::vector<int32_t> ctile(At.nnz());
-    std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
-    for (int64_t i = 0; i < m; i++)
-      for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) ctile[fill[At.col[q]]++] = tile[i];
-    std::vector<int> uniq;
-    for (int64_t c = 0; c < m; c++) {
-      if (!shared[c]) continue;
-      uniq.assign(ctile.begin() + cptr[c], ctile.begin() + cptr[c + 1]);
-      std::sort(uniq.begin(), uniq.end());
-      uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-      for (size_t x = 0; x < uniq.size(); x++)
-        for (size_t y = 0; y < uniq.size(); y++)
-          if (x != y) nbs[uniq[x]].insert(uniq[y]);
-    }
-  }
-  std::vector<int> nbr((size_t)T * kNbMax, -1);
-  for (int t = 0; t < T; t++) {
-    if ((int)nbs[t].size() > kNbMax) {
-      why = "tile " + std::to_string(t) + " has " + std::to_string(nbs[t].size()) + " neighbour tiles (> " +
-            std::to_string(kNbMax) + ")";
-      return false;
-    }
-    int j = 0;
-    for (int n : nbs[t]) nbr[(size_t)t * kNbMax + j++] = n;
-  }
   // rows: interior (all columns private) or boundary
   std::vector<uint8_t> boundary(m, 0);
   int64_t n_private_nnz = 0, n_interior = 0;
   for (int64_t i = 0; i < m; i++) {
+    const int64_t len = At.ptr[i + 1] - At.ptr[i];
+    if (len > 65535 || SliceLayout(1, (int)len, true).bytes > kSlot) {
+      why = "row " + std::to_string(i) + " (" + std::to_string(len) + " nonzeros) is too long for one " +
+            std::to_string(kSlot) + "-byte slice";
+      return false;
+    }
     for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) {
       if (shared[At.col[q]]) boundary[i] = 1;
       else n_private_nnz++;
     }
     n_interior += !boundary[i];
   }
-  // tasks and chunks, tile by tile (interior rows first within a task)
+  // tasks (tile, step): boundary slices first, then interior slices; each group is sorted by
+  // decreasing row length (then row id) and cut into slices of <= 32 rows (ELL inside a slice)
   std::vector<std::vector<std::vector<int32_t>>> rows_tk(T);
   for (int t = 0; t < T; t++) rows_tk[t].resize(p.nsteps);
-  for (int k = 0; k < p.nsteps; k++) {
-    for (int pass = 0; pass < 2; pass++)
-      for (int q = p.sched.step_ptr[k]; q < p.sched.step_ptr[k + 1]; q++) {
-        const int32_t r = p.sched.rows[q];
-        if (boundary[r] == pass) rows_tk[tile[r]][k].push_back(r);
-      }
-  }
-  std::vector<ChunkMeta> meta;
-  std::vector<TaskMeta> tmeta;
-  std::vector<int> tile_chunk(T + 1, 0), tile_task(T + 1, 0), k_first(T, p.nsteps);
-  std::vector<std::vector<int32_t>> chunk_rows;
+  for (int k = 0; k < p.nsteps; k++)
+    for (int q = p.sched.step_ptr[k]; q < p.sched.step_ptr[k + 1]; q++) {
+      const int32_t r = p.sched.rows[q];
+      rows_tk[tile[r]][k].push_back(r);
+    }
+  auto rlen = [&](int32_t r) { return (int)(At.ptr[r + 1] - At.ptr[r]); };
+  std::vector<int4> smeta, cmeta, tmeta;
+  std::vector<int> tile_slice(T + 1, 0), tile_chunk(T + 1, 0), tile_task(T + 1, 0);
+  std::vector<std::vector<int32_t>> slice_rows;  // global slice order
+  std::vector<int64_t> slice_pos;                // byte offset of each slice in the stream
+  std::vector<uint8_t> slice_bnd;
+  std::vector<int64_t> mb_of_row(m, -1);         // boundary rows: mailbox index of entry 0
+  std::vector<int32_t> R_of_row(m, 0);
+  long long off = 0, pad = 0, NB = 0;
+  int nsl_max = 1, nck_max = 1, ntask_max = 1;
   for (int t = 0; t < T; t++) {
-    std::vector<int> tasks;
-    for (int k = 0; k < p.nsteps; k++)
-      if (!rows_tk[t][k].empty()) tasks.push_back(k);
-    if (!tasks.empty()) k_first[t] = tasks[0];
-    for (size_t ti = 0; ti < tasks.size(); ti++) {
-      const int k = tasks[ti];
-      TaskMeta tm{};
-      tm.step = k;
-      tm.k_next = ti + 1 < tasks.size() ? tasks[ti + 1] : p.nsteps + tasks[0];
-      tm.boundary = 0;
-      const auto& rs = rows_tk[t][k];
-      size_t a = 0;
-      while (a < rs.size()) {
-        const uint8_t kind = boundary[rs[a]];
-        size_t b = a;
-        int nnz = 0;
-        while (b < rs.size() && boundary[rs[b]] == kind) {
-          const int len = (int)(At.ptr[rs[b] + 1] - At.ptr[rs[b]]);
-          if (ChunkLayout((int)(b - a + 1), nnz + len).bytes > kChunkCap || nnz + len > kEPT * kNCW * 32) break;
-          nnz += len;
-          b++;
+    const int sl0 = (int)smeta.size();
+    int chunk_local = -1, chunk_bytes = kSlot;  // force a new chunk for the tile's first slice
+    const long long tile_base = off;
+    for (int k = 0; k < p.nsteps; k++) {
+      if (rows_tk[t][k].empty()) continue;
+      int cnt[2] = {0, 0};
+      const int first = (int)smeta.size() - sl0;
+      for (int kind = 0; kind < 2; kind++) {  // 0: boundary, 1: interior
+        const bool bnd = kind == 0;
+        std::vector<int32_t> g;
+        for (int32_t r : rows_tk[t][k])
+          if (boundary[r] == (uint8_t)bnd) g.push_back(r);
+        std::stable_sort(g.begin(), g.end(), [&](int32_t x, int32_t y) { return rlen(x) > rlen(y); });
+        size_t a = 0;
+        while (a < g.size()) {
+          const int W = rlen(g[a]);
+          size_t b = a;
+          while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
+          const int R = (int)(b - a), bytes = SliceLayout(R, W, bnd).bytes;
+          for (size_t r = a; r < b; r++) pad += W - rlen(g[r]);
+          if (chunk_bytes + bytes > kSlot) {  // open a new chunk
+            chunk_local++;
+            chunk_bytes = 0;
+            cmeta.push_back(make_int4((int)(off - tile_base), 0, 0, 0));
+          }
+          if (chunk_local >= (1 << 20)) { why = "too many chunks in tile " + std::to_string(t); return false; }
+          int mbase = 0;
+          if (bnd) {
+            if (NB + (long long)W * R >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
+            mbase = (int)NB;
+            for (int r = 0; r < R; r++) {
+              mb_of_row[g[a + r]] = NB + r;
+              R_of_row[g[a + r]] = R;
+            }
+            NB += (long long)W * R;
+          }
+          smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W, mbase));
+          slice_rows.emplace_back(g.begin() + a, g.begin() + b);
+          slice_pos.push_back(off);
+          slice_bnd.push_back(bnd);
+          cmeta.back().y += bytes;
+          cmeta.back().z += 1;
+          chunk_bytes += bytes;
+          off += bytes;
+          cnt[kind]++;
+          a = b;
         }
-        if (b == a) {
-          why = "row " + std::to_string(rs[a]) + " is too long for one " + std::to_string(kChunkCap) + "-byte chunk";
-          return false;
-        }
-        ChunkMeta mt{};
-        mt.rows = (int)(b - a);
-        mt.nnz = nnz;
-        mt.task = (int)ti;
-        mt.flags = 0;
-        if (kind == 1 && !tm.boundary) { mt.flags |= kFirstBoundary; tm.boundary = 1; }
-        if (b == rs.size()) mt.flags |= kLastOfTask;
-        meta.push_back(mt);
-        chunk_rows.emplace_back(rs.begin() + a, rs.begin() + b);
-        a = b;
       }
-      tmeta.push_back(tm);
+      if (cnt[0] > 0xffff || cnt[1] > 0x7fff) { why = "too many slices in one task"; return false; }
+      tmeta.push_back(make_int4(first, cnt[0] | (cnt[1] << 16), k, 0));
     }
-    tile_chunk[t + 1] = (int)meta.size();
+    tile_slice[t + 1] = (int)smeta.size();
+    tile_chunk[t + 1] = (int)cmeta.size();
     tile_task[t + 1] = (int)tmeta.size();
-    if (tile_chunk[t + 1] - tile_chunk[t] > kMaxChunks) {
-      why = "tile " + std::to_string(t) + " needs more than " + std::to_string(kMaxChunks) + " chunks";
-      return false;
+    nsl_max = std::max(nsl_max, tile_slice[t + 1] - tile_slice[t]);
+    nck_max = std::max(nck_max, tile_chunk[t + 1] - tile_chunk[t]);
+    ntask_max = std::max(ntask_max, tile_task[t + 1] - tile_task[t]);
+  }
+  const size_t meta_bytes = 16 * ((size_t)nsl_max + nck_max + ntask_max);
+  if (meta_bytes > (size_t)kMetaBudget) {
+    why = "K2 metadata (" + std::to_string(meta_bytes) + " B per tile) exceeds its shared-memory budget";
+    return false;
+  }
+  // Bank-aware placement of the private x~ in shared memory.  A warp's access to entry j of its
+  // slice touches one 8-byte word per lane; words w and w' conflict when w = w' (mod 16) (same
+  // bank pair), and the access takes max over residues of the number of distinct words, >= 2.
+  // Random placement costs ~5; here each tile's private columns get residues greedily (most
+  // accessed first), each residue chosen to minimise the column's collisions with the residues
+  // already in its access groups, under a per-residue capacity; local index = residue + 16 * rank.
+  {
+    std::vector<int32_t> row_of_slice_lane;  // scratch
+    pmap.clear();
+    for (int t = 0; t < T; t++) {
+      const int b = pmap_ptr[t], e = pmap_ptr[t + 1], n = e - b;
+      pmap_ptr[t] = (int)pmap.size();
+      if (n == 0) { np_t[t] = 0; continue; }
+      // access groups of this tile: (slice, j); member lists per private column (by old local index)
+      std::vector<int32_t> cols(n);
+      std::vector<std::vector<int32_t>> groups_of(n);
+      int ng = 0;
+      for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
+        const auto& rows = slice_rows[si];
+        const int W = smeta[si].z;
+        for (int j = 0; j < W; j++, ng++)
+          for (int32_t i : rows)
+            if (j < rlen(i)) {
+              const int32_t cg = At.col[At.ptr[i] + j];
+              if (!shared[cg]) groups_of[local[cg]].push_back(ng);
+            }
+      }
+      std::vector<int32_t> gl;  // old local -> global column
+      gl.resize(n);
+      for (int64_t c = 0; c < m; c++)
+        if (!shared[c] && col_tile[c] == t && local[c] >= 0) gl[local[c]] = (int32_t)c;
+      std::vector<int> order(n);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return groups_of[x].size() > groups_of[y].size(); });
+      const int cap = (int)((n + 15) / 16 * 1.03) + 1;
+      std::vector<uint8_t> cnt((size_t)ng * 16, 0);
+      std::vector<int> csize(16, 0);
+      std::vector<int> res(n, 0);
+      for (int x : order) {
+        int best = -1;
+        long cost_best = 1L << 60;
+        for (int k = 0; k < 16; k++) {
+          if (csize[k] >= cap) continue;
+          long cost = 0;
+          for (int g : groups_of[x]) cost += cnt[(size_t)g * 16 + k];
+          cost = cost * 64 + csize[k] * 64 / cap;  // tie-break towards emptier residues
+          if (cost < cost_best) { cost_best = cost; best = k; }
+        }
+        res[x] = best;
+        csize[best]++;
+        for (int g : groups_of[x]) cnt[(size_t)g * 16 + best]++;
+      }
+      int mx = 0;
+      for (int k = 0; k < 16; k++) mx = std::max(mx, csize[k]);
+      np_t[t] = 16 * mx;
+      std::vector<int> rank(16, 0);
+      std::vector<int> slot_col((size_t)16 * mx, -1);
+      for (int x = 0; x < n; x++) {
+        const int li = res[x] + 16 * rank[res[x]]++;
+        slot_col[li] = gl[x];
+      }
+      for (int li = 0; li < 16 * mx; li++) {
+        if (slot_col[li] >= 0) local[slot_col[li]] = li;
+        pmap.push_back(slot_col[li]);  // -1: a hole (x~ = x~* = 0, never accessed)
+      }
+    }
+    pmap_ptr[T] = (int)pmap.size();
+  }
+  const int np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
+  const size_t base_smem = fixed + meta_bytes + 16 * ((size_t)np_max + 1);  // + the zero slot
+  const int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
+  if (NS < kMinSlots) { why = "shared memory too small for the TMA ring"; return false; }
+
+  // the version chain of every shared column c: the rows touching c in schedule (step) order; the
+  // value written by the p-th goes to the (p+1)-th's mailbox slot, the last one's (kWrap) to the
+  // first one's slot of the next sweep and to x~.  mout[row entry] = target slot.
+  std::vector<unsigned> mout_of_entry(At.nnz(), 0u);
+  std::vector<int> seed_idx, seed_col;
+  std::vector<int> lastcol_ptr(T + 1, 0), lastcol;
+  {
+    std::vector<int64_t> cptr(m + 1, 0);
+    for (int64_t q = 0; q < At.nnz(); q++) cptr[At.col[q] + 1]++;
+    for (int64_t c = 0; c < m; c++) cptr[c + 1] += cptr[c];
+    std::vector<int64_t> ent(At.nnz());  // entries (CSR positions) of each column
+    {
+      std::vector<int64_t> fill(cptr.begin(), cptr.end() - 1);
+      for (int64_t i = 0; i < m; i++)
+        for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) ent[fill[At.col[q]]++] = q;
+    }
+    std::vector<int32_t> row_of_entry(At.nnz());
+    for (int64_t i = 0; i < m; i++)
+      for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) row_of_entry[q] = (int32_t)i;
+    auto slot_of = [&](int64_t q) {  // mailbox slot of CSR entry q (its row is a boundary row)
+      const int32_t i = row_of_entry[q];
+      return mb_of_row[i] + (q - At.ptr[i]) * R_of_row[i];
+    };
+    std::vector<std::vector<int>> per(T);
+    std::vector<int64_t> ch;
+    for (int64_t c = 0; c < m; c++) {
+      if (!shared[c]) continue;
+      ch.assign(ent.begin() + cptr[c], ent.begin() + cptr[c + 1]);
+      std::sort(ch.begin(), ch.end(), [&](int64_t x, int64_t y) { return step_of[row_of_entry[x]] < step_of[row_of_entry[y]]; });
+      for (size_t pidx = 0; pidx < ch.size(); pidx++) {
+        const bool last = pidx + 1 == ch.size();
+        const int64_t tgt = slot_of(ch[last ? 0 : pidx + 1]);
+        mout_of_entry[ch[pidx]] = (unsigned)tgt | (last ? kWrap : 0u);
+      }
+      seed_idx.push_back((int)slot_of(ch[0]));
+      seed_col.push_back((int)c);
+      per[tile[row_of_entry[ch.back()]]].push_back((int)c);
+    }
+    for (int t = 0; t < T; t++) {
+      lastcol_ptr[t + 1] = lastcol_ptr[t] + (int)per[t].size();
+      lastcol.insert(lastcol.end(), per[t].begin(), per[t].end());
     }
   }
-  // stream bytes
-  long long off = 0;
-  for (auto& mt : meta) {
-    mt.off = off;
-    off += ChunkLayout(mt.rows, mt.nnz).bytes;
-  }
+
+  // the stream: slices in tile, task, kind order; ELL inside a slice
   std::vector<unsigned char> stream(off, 0);
   std::vector<int32_t> orig_q;
   std::vector<int64_t> fslot;
-  std::vector<double> nrm2(m);
-  for (int64_t i = 0; i < m; i++) {
-    double s = 0.0;
-    for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) s = s + At.val[q] * At.val[q];
-    nrm2[i] = s;
-  }
-  p.tile_of_row.assign(tile.begin(), tile.end());
-  for (size_t c = 0; c < meta.size(); c++) {
-    const ChunkMeta& mt = meta[c];
-    const ChunkLayout L(mt.rows, mt.nnz);
-    unsigned char* blk = stream.data() + mt.off;
-    double* val = (double*)(blk + L.o_val);
-    double* nv = (double*)(blk + L.o_n);
+  orig_q.reserve(m);
+  fslot.reserve(m);
+  for (size_t si = 0; si < slice_rows.size(); si++) {
+    const auto& rows = slice_rows[si];
+    const int R = (int)rows.size(), W = smeta[si].z;
+    const bool bnd = slice_bnd[si];
+    const SliceLayout L(R, W, bnd);
+    unsigned char* blk = stream.data() + slice_pos[si];
+    double* val = (double*)blk;
+    double* fv = (double*)(blk + L.o_f);
     unsigned* col = (unsigned*)(blk + L.o_col);
-    int* rp = (int*)(blk + L.o_rp);
-    int w = 0;
-    rp[0] = 0;
-    for (int r = 0; r < mt.rows; r++) {
-      const int32_t i = chunk_rows[c][r];
-      for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++, w++) {
+    unsigned* mout = (unsigned*)(blk + L.o_mout);
+    unsigned short* len = (unsigned short*)(blk + L.o_len);
+    for (int r = 0; r < R; r++) {
+      const int32_t i = rows[r];
+      for (int j = 0; j < rlen(i); j++) {
+        const int64_t q = At.ptr[i] + j;
         const int32_t cg = At.col[q];
-        unsigned e = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
-        if (last_row[cg] == i) e |= kLast;
-        col[w] = e;
-        val[w] = At.val[q];
+        col[j * R + r] = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
+        val[j * R + r] = At.val[q];
+        if (bnd) mout[j * R + r] = shared[cg] ? mout_of_entry[q] : 0u;
       }
-      rp[r + 1] = w;
-      nv[r] = nrm2[i];
+      for (int j = rlen(i); j < W; j++) col[j * R + r] = (unsigned)np_max;  // ELL padding: zero slot, value +0
+      len[r] = (unsigned short)rlen(i);
+      fv[r] = 0.0;  // f~ is scattered in per solve (k2_scatter_f)
       orig_q.push_back(p.perm[i]);
-      fslot.push_back((mt.off + L.o_f) / 8 + r);
+      fslot.push_back((slice_pos[si] + L.o_f) / 8 + r);
     }
   }
+  p.tile_of_row.assign(tile.begin(), tile.end());
+
   // upload
   K2Plan* k = new K2Plan();
   p.k2 = k;
   k->T = T;
-  int nck_max = 1, ntask_max = 1;
-  for (int t = 0; t < T; t++) {
-    nck_max = std::max(nck_max, tile_chunk[t + 1] - tile_chunk[t]);
-    ntask_max = std::max(ntask_max, tile_task[t + 1] - tile_task[t]);
-  }
+  k->NS = NS;
+  k->nsl_max = nsl_max;
   k->nck_max = nck_max;
   k->ntask_max = ntask_max;
-  k->np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
-  k->smem = fixed + 16 * (size_t)nck_max + 4 * (size_t)((nck_max + 3) & ~3) + 16 * (size_t)ntask_max +
-            16 * (size_t)k->np_max;
+  k->np_max = np_max;
+  k->smem = (size_t)NS * kSlot + base_smem;
+  k->NB = NB;
+  k->nseed = (int)seed_idx.size();
   std::vector<long long> tile_off(T, 0);
-  for (int t = 0; t < T; t++) tile_off[t] = tile_chunk[t] < (int)meta.size() ? meta[tile_chunk[t]].off : 0;
+  {
+    int ci = 0;
+    long long pos = 0;
+    for (int t = 0; t < T; t++) {
+      tile_off[t] = pos;
+      for (; ci < tile_chunk[t + 1]; ci++) pos += cmeta[ci].y;
+    }
+  }
   k->private_frac = p.nnz ? (double)n_private_nnz / (double)p.nnz : 0.0;
   k->interior_frac = (double)n_interior / (double)m;
   k->stream_bytes = off;
-  k->nchunks = (int)meta.size();
+  k->pad_entries = pad;
+  k->nchunks = (int)cmeta.size();
+  k->ntask_total = (int)tmeta.size();
   cudaError_t e = cudaSuccess;
 #define K2_UP(dst, src, n) \
   if (e == cudaSuccess) e = k2_upload(*k, dst, src, n)
   K2_UP(&k->stream, stream.data(), stream.size());
   K2_UP(&k->tile_off, tile_off.data(), tile_off.size());
-  K2_UP(&k->meta, meta.data(), meta.size());
+  K2_UP(&k->smeta, smeta.data(), smeta.size());
+  K2_UP(&k->cmeta, cmeta.data(), cmeta.size());
   K2_UP(&k->tmeta, tmeta.data(), tmeta.size());
+  K2_UP(&k->tile_slice, tile_slice.data(), tile_slice.size());
   K2_UP(&k->tile_chunk, tile_chunk.data(), tile_chunk.size());
   K2_UP(&k->tile_task, tile_task.data(), tile_task.size());
-  K2_UP(&k->nbr, nbr.data(), nbr.size());
   K2_UP(&k->pmap_ptr, pmap_ptr.data(), pmap_ptr.size());
   K2_UP(&k->pmap, pmap.data(), pmap.size());
-  K2_UP(&k->k_first, k_first.data(), k_first.size());
+  K2_UP(&k->lastcol_ptr, lastcol_ptr.data(), lastcol_ptr.size());
+  K2_UP(&k->lastcol, lastcol.data(), lastcol.size());
+  K2_UP(&k->seed_idx, seed_idx.data(), seed_idx.size());
+  K2_UP(&k->seed_col, seed_col.data(), seed_col.size());
+  K2_UP(&k->mbox, (unsigned long long*)nullptr, 2 * (size_t)std::max<long long>(NB, 1));
   K2_UP(&k->orig_q, orig_q.data(), orig_q.size());
   K2_UP(&k->fslot, fslot.data(), fslot.size());
-  K2_UP(&k->progress, (int*)nullptr, (size_t)T * kFlagStride);
   K2_UP(&k->sync, (SyncState*)nullptr, 1);
   K2_UP(&k->partials, (double*)nullptr, 2 * (size_t)T);
 #undef K2_UP
@@ -891,57 +1122,72 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   cudaError_t e;
   k2_scatter_f<<<(int)std::min<int64_t>((p.m + 255) / 256, 148 * 8), 256, 0, s>>>(p.m, k.orig_q, k.fslot, f_user,
                                                                                   (double*)k.stream);
-  k2_reset<<<1, 256, 0, s>>>(k.T, k.k_first, k.progress, k.sync);
-  launches += 2;
+  k2_reset<<<1, 1, 0, s>>>(k.sync);
+  k2_mbox_fill<<<148 * 4, 256, 0, s>>>(k.mbox, 2 * std::max<long long>(k.NB, 1));
+  k2_mbox_seed<<<std::max(1, std::min(148 * 4, (k.nseed + 255) / 256)), 256, 0, s>>>(k.mbox, k.nseed, k.seed_idx, k.seed_col,
+                                                                                      p.d_xt);
+  launches += 4;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   K2Args a;
   a.stream = k.stream;
   a.tile_off = k.tile_off;
-  a.meta = k.meta;
+  a.smeta = k.smeta;
+  a.tile_slice = k.tile_slice;
+  a.cmeta = k.cmeta;
   a.tile_chunk = k.tile_chunk;
   a.tmeta = k.tmeta;
   a.tile_task = k.tile_task;
-  a.nbr = k.nbr;
   a.pmap_ptr = k.pmap_ptr;
   a.pmap = k.pmap;
+  a.lastcol_ptr = k.lastcol_ptr;
+  a.lastcol = k.lastcol;
+  a.mbox = k.mbox;
+  a.NB = k.NB;
   a.xg = p.d_xt;
   a.xst = p.d_xst;
-  a.progress = k.progress;
   a.sync = k.sync;
   a.partials = k.partials;
   a.ctrl = p.d_ctrl;
-  a.nsteps = p.nsteps;
   a.T = k.T;
+  a.NS = k.NS;
+  a.nsl_max = k.nsl_max;
   a.nck_max = k.nck_max;
   a.ntask_max = k.ntask_max;
   a.np_max = k.np_max;
-  static const int dbg = getenv("POBK_K2_DEBUG") ? atoi(getenv("POBK_K2_DEBUG")) : 0;
-  a.debug = dbg;
-  a.prof = nullptr;
-  static const bool prof_on = getenv("POBK_K2_PROFILE") != nullptr;
-  if (prof_on) {
-    if (!k.prof) cudaMalloc(&k.prof, (size_t)k.T * 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(k.prof, 0, (size_t)k.T * 16 * sizeof(unsigned long long), s);
-    a.prof = k.prof;
+  a.trace = nullptr;
+  a.trace_sweep = -1;
+  static const char* trace_env = getenv("POBK_K2_TRACE");
+  if (trace_env) {
+    const size_t n = (size_t)k.T * k.ntask_max * 12;
+    if (!k.trace) cudaMalloc(&k.trace, n * sizeof(unsigned long long));
+    cudaMemsetAsync(k.trace, 0, n * sizeof(unsigned long long), s);
+    a.trace = k.trace;
+    a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
   const void* fn = (const void*)k2_sweeps;
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(kNT), args, k.smem, s);
   launches++;
-  if (e == cudaSuccess && a.prof) {
-    std::vector<unsigned long long> h((size_t)k.T * 16);
+  if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py
+    const size_t n = (size_t)k.T * k.ntask_max * 12;
+    std::vector<unsigned long long> h(n);
     cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    double sum[11] = {0}, mx[11] = {0};
-    for (int t = 0; t < k.T; t++)
-      for (int j = 0; j < 11; j++) { sum[j] += (double)h[t * 16 + j]; mx[j] = std::max(mx[j], (double)h[t * 16 + j]); }
-    fprintf(stderr, "[k2 prof] phases (mean per tile): A %.3g barA %.3g B %.3g barB %.3g C %.3g\n", sum[6] / k.T,
-            sum[7] / k.T, sum[8] / k.T, sum[9] / k.T, sum[10] / k.T);
-    fprintf(stderr, "[k2 prof] warp0 cycles per tile (mean/max): go %.3g/%.3g full %.3g/%.3g taskbar %.3g/%.3g "
-                    "epoch %.3g/%.3g total %.3g/%.3g chunks %.0f\n",
-            sum[0] / k.T, mx[0], sum[1] / k.T, mx[1], sum[2] / k.T, mx[2], sum[3] / k.T, mx[3], sum[4] / k.T, mx[4],
-            sum[5] / k.T);
+    cudaMemcpy(h.data(), a.trace, n * 8, cudaMemcpyDeviceToHost);
+    std::vector<int4> tm(k.ntask_total);
+    std::vector<int> tt(k.T + 1);
+    cudaMemcpy(tm.data(), k.tmeta, tm.size() * sizeof(int4), cudaMemcpyDeviceToHost);
+    cudaMemcpy(tt.data(), k.tile_task, tt.size() * sizeof(int), cudaMemcpyDeviceToHost);
+    const char* path = getenv("POBK_K2_TRACE_OUT") ? getenv("POBK_K2_TRACE_OUT") : "k2_trace.bin";
+    FILE* fp = fopen(path, "wb");
+    if (fp) {
+      int hdr[4] = {k.T, k.ntask_max, 12, k.ntask_total};
+      fwrite(hdr, sizeof(hdr), 1, fp);
+      fwrite(h.data(), 8, n, fp);
+      fwrite(tm.data(), sizeof(int4), tm.size(), fp);
+      fwrite(tt.data(), sizeof(int), tt.size(), fp);
+      fclose(fp);
+    }
   }
   return e;
 }
@@ -949,7 +1195,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
 void k2_free(Plan& p) {
   if (!p.k2) return;
   for (void* v : p.k2->allocs) cudaFree(v);
-  if (p.k2->prof) cudaFree(p.k2->prof);
+  if (p.k2->trace) cudaFree(p.k2->trace);
   delete p.k2;
   p.k2 = nullptr;
 }
