@@ -11,12 +11,12 @@ import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libpobk.so")
-BUILD = os.path.join(HERE, "_build")
+OUT = os.environ.get("POBK_BUILD_OUT", os.path.join(HERE, "libpobk.so"))  # development variants build elsewhere
+BUILD = os.environ.get("POBK_BUILD_DIR", os.path.join(HERE, "_build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [f"-DPOBK_K2_MAXJ={os.environ.get('POBK_K2_MAXJ', '24')}", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
-          "-I" + os.path.join(HERE, "..", "include")]
+          "-I" + os.path.join(HERE, "..", "include")] + os.environ.get("POBK_EXTRA_FLAGS", "").split()
 
 SOURCES = [
     "host/preprocess.cpp",

@@ -33,8 +33,10 @@
 //    which never touches x~.
 //  * The RSE is evaluated at the end of each sweep by each tile over the columns
 //    it owns (its private ones in shared memory, and the shared ones whose last writer in the
-//    sweep it holds; that writer also stores the value to x~ in global memory).  Partials are
-//    combined in fixed orders; one grid-wide decision per sweep.
+//    sweep it holds, read from the wrap mailbox slot).  Partials are combined in fixed orders;
+//    one grid-wide decision per sweep.
+//  * Warps 0, 4, 8, 12 (one SM sub-partition) take the boundary slices -- the critical path --
+//    and do not share issue slots with the interior slices, taken by the other 11 compute warps.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,6 +58,8 @@ constexpr int kNT = 512;            // threads per CTA (one CTA per SM)
 constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
 constexpr int kNC = kNCW * 32;      // compute threads
 constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
+constexpr int kBndWarps = (kNCW + 3) / 4;    // warps 0, 4, 8, 12 (one SM sub-partition): boundary slices
+constexpr int kIntWarps = kNCW - kBndWarps;  // the other compute warps: interior slices
 constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
 constexpr int kMinSlots = 4, kMaxSlots = 12;
 constexpr int kSliceRows = 32;      // rows per slice (one lane each)
@@ -107,6 +111,7 @@ struct K2Args {
   const int* pmap;            // private columns (global ids), tile by tile
   const int* lastcol_ptr;     // [T+1]
   const int* lastcol;         // shared columns whose last writer in a sweep is in the tile, tile by tile
+  const int* lastslot;        // ... and their wrap mailbox slot (the next sweep's first reader's)
   unsigned long long* mbox;   // [2*NB] mailboxes (fp64 bits or kSentinel), parity-major
   long long NB;
   double* xg;                 // x~ (RCM frame): x0 in, final out; shared columns' sweep-final values
@@ -251,12 +256,15 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
     for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
     for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    // entries past the slice width contribute +0 * +0 (bit-exact no-ops): no per-entry branches,
+    // so the next batch's loads can issue under this batch's arithmetic
 #pragma unroll
-    for (int u = 0; u < kBatch; u++)
-      if (jb + u < W) {
-        s = __dadd_rn(s, __dmul_rn(av[u], xv[u]));
-        n2 = __dadd_rn(n2, __dmul_rn(av[u], av[u]));
-      }
+    for (int u = 0; u < kBatch; u++) {
+      const bool in = jb + u < W;
+      const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
+      s = __dadd_rn(s, __dmul_rn(a, x));
+      n2 = __dadd_rn(n2, __dmul_rn(a, a));
+    }
   }
   const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
   for (int jb = 0; jb < W; jb += kBatch) {
@@ -277,8 +285,9 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
 // boundary slice, in two halves: pre() loads the PRIVATE x~ (final for this step as soon as the
 // tile's previous task is done) and notes the shared entries; post() polls the shared entries'
 // mailboxes (this lane's slot of entry j: mbox_in + j*R), re-arms them, applies the rows, writes
-// private results to shared memory and shared results to their consumers' mailboxes (and, for a
-// sweep's last writer, to x~ in global memory).
+// private results to shared memory and shared results to their consumers' mailboxes.  (A sweep's
+// last writer of a column writes the next sweep's first reader's slot, which therefore holds the
+// column's sweep-final value until that reader runs: the RSE and the final write-back read it.)
 struct BSlice {
   double xr[kMaxJ];
   unsigned shm;  // bit j: entry j (< kMaxJ) is a shared column of this lane's row
@@ -287,14 +296,15 @@ struct BSlice {
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
       if (jb < W) {
-        unsigned c[kBatch];
+        unsigned cr[kBatch];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+        for (int u = 0; u < kBatch; u++) cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {
-          const bool sh = (c[u] & kShared) && jb + u < S.myl;
+          const unsigned c = cr[u];
+          const bool sh = (c & kShared) && jb + u < S.myl;
           shm |= sh ? (1u << (jb + u)) : 0u;
-          xr[jb + u] = (c[u] & kShared) ? 0.0 : lds64(xb + 8u * c[u]);
+          xr[jb + u] = ((c & kShared) || jb + u >= W) ? 0.0 : lds64(xb + 8u * c);
         }
       }
     }
@@ -325,19 +335,22 @@ struct BSlice {
 #pragma unroll
     for (int j = 0; j < kMaxJ; j++) stm_if((shm >> j) & 1u, mbox_in + (size_t)j * R, kSentinel);
   }
-  __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, double* xg, unsigned long long* mbox_in,
-                                       unsigned long long* mbox_p, unsigned long long* mbox_q, int R) {
+  // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
+  __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
+                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, int R,
+                                       unsigned long long* trp) {
     double s = 0.0, n2 = 0.0;
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
       if (jb < W) {
+        double av[kBatch];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++)
-          if (jb + u < W) {
-            const double a = lds64(S.vb + (jb + u) * S.vs);
-            s = __dadd_rn(s, __dmul_rn(a, xr[jb + u]));
-            n2 = __dadd_rn(n2, __dmul_rn(a, a));
-          }
+        for (int u = 0; u < kBatch; u++) av[u] = jb + u < W ? lds64(S.vb + min(jb + u, W - 1) * S.vs) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {  // past the width: +0 * +0 (xr, av are +0 there)
+          s = __dadd_rn(s, __dmul_rn(av[u], xr[jb + u]));
+          n2 = __dadd_rn(n2, __dmul_rn(av[u], av[u]));
+        }
       }
     }
     for (int j = kMaxJ; j < W; j++) {
@@ -356,22 +369,45 @@ struct BSlice {
       s = __dadd_rn(s, __dmul_rn(a, x));
       n2 = __dadd_rn(n2, __dmul_rn(a, a));
     }
+    if (trp) {
+      double s2 = s;
+      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
+    }
     const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+    if (trp) {
+      double a2 = alpha;
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[9] = gtimer();
+    }
 #pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // new x~ (in place)
       if (jb < W) {
+        double av[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) xr[jb + u] = __dadd_rn(xr[jb + u], __dmul_rn(alpha, av[u]));
+      }
+    }
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // write back: a batch of mailbox targets, then its stores
+      if (jb < W) {
+        unsigned mo[kBatch], cr[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+          mo[u] = lds32(S.mb + min(jb + u, W - 1) * S.cs);
+        }
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {
           const int j = jb + u;
-          const unsigned jj = (unsigned)min(j, W - 1);
-          const unsigned c = lds32(S.cb + jj * S.cs);
-          const double x1 = __dadd_rn(xr[j], __dmul_rn(alpha, lds64(S.vb + jj * S.vs)));
           const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
-          sts64_if(act & (sh ^ 1u), xb + 8u * (c & kIdx), x1);
-          const unsigned mo = lds32(S.mb + jj * S.cs);
-          const unsigned long long bits = (unsigned long long)__double_as_longlong(x1);
-          stm_if(act & sh, ((mo & kWrap) ? mbox_q : mbox_p) + (mo & ~kWrap), bits);
-          if (act & sh & (mo >> 31)) st_cg(xg + (c & kIdx), x1);  // the sweep's last writer of c
+          sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
+          stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
+                 (unsigned long long)__double_as_longlong(xr[j]));
         }
       }
     }
@@ -384,8 +420,7 @@ struct BSlice {
         {
           const double x1 = __dadd_rn(__longlong_as_double((long long)w), __dmul_rn(alpha, a));
           const unsigned mo = lds32(S.mb + j * S.cs);
-          stm_if(1u, ((mo & kWrap) ? mbox_q : mbox_p) + (mo & ~kWrap), (unsigned long long)__double_as_longlong(x1));
-          if (mo & kWrap) st_cg(xg + idx, x1);
+          stm_if(1u, mbox + ((mo & ~kWrap) + ((mo & kWrap) ? off_q : off_p)), (unsigned long long)__double_as_longlong(x1));
         }
       } else if (!(cj & kShared) && j < S.myl) {
         const unsigned ca = xb + 8u * idx;
@@ -470,22 +505,25 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const unsigned ring_s = opaque(smem_u32(ring));
     long long sweep = 0;
     while (sweep < maxs) {
-      unsigned long long* const mbox_p = a.mbox + (size_t)(sweep & 1) * a.NB;        // this sweep's slots
-      unsigned long long* const mbox_q = a.mbox + (size_t)((sweep + 1) & 1) * a.NB;  // the next sweep's
+      const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
+      unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
       for (int ti = 0; ti < ntask; ti++) {
         const int4 tm = tmeta[ti];
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
         unsigned long long* trp = tr ? a.trace + ((size_t)t * a.ntask_max + ti) * 12 : nullptr;
         if (tr && warp == 0 && lane == 0) trp[0] = gtimer();
-        for (int q = warp; q < ntot; q += kNCW) {
-          const bool bnd = q < nbnd;
+        // boundary slices on warps 0, 4, 8, 12 (sub-partition 0), interior ones on the other 11
+        const bool bw = (warp & 3) == 0;
+        const int q_first = bw ? (warp >> 2) : nbnd + (warp - (warp >> 2) - 1);
+        const int q_step = bw ? kBndWarps : kIntWarps, q_end = bw ? nbnd : ntot;
+        for (int q = q_first; q < q_end; q += q_step) {
+          const bool bnd = bw;
           const int4 sl = smeta[tm.x + q];
           const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
           const unsigned long long g = (unsigned long long)sweep * nck + chunk;
           const int slot = (int)(g % (unsigned)NS);
-          while (ld_vol_shared64(&ctl->issued) <= g) {
-          }
+          while (ld_vol_shared64(&ctl->issued) <= g) __nanosleep(32);  // ring full: let the others use the smem pipe
           mbar_wait(&ctl->full[slot], (unsigned)((g / (unsigned)NS) & 1));
           const unsigned blk = ring_s + (unsigned)(slot * kSlot + sl.y);
           if (tr && lane == 0 && (q == 0 || q == nbnd)) trp[q == 0 ? 4 : 6] = gtimer();
@@ -497,7 +535,11 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             unsigned long long* const mbox_in = mbox_p + sl.w + (lane < R ? lane : 0);
             B.poll(S, W, R, mbox_in);
             if (tr && q == 0 && lane == 0) trp[1] = gtimer();
-            B.post(S, W, xb, a.xg, mbox_in, mbox_p, mbox_q, R);
+            B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
+            if (tr && q == 0) {
+              __syncwarp();
+              if (lane == 0) trp[10] = gtimer();
+            }
           } else {
             slice_interior(S, W, xb);
           }
@@ -520,9 +562,10 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           const double d = xloc[j] - xsloc[j];
           acc = fma(d, d, acc);
         }
+        const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB;  // sweep = sweeps done
         for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNC) {
-          const int c = a.lastcol[j];
-          const double d = ld_cg(a.xg + c) - __ldg(a.xst + c);
+          const unsigned long long w = ldm_if(1u, wrap + a.lastslot[j], 0ull);
+          const double d = __longlong_as_double((long long)w) - __ldg(a.xst + a.lastcol[j]);
           acc = fma(d, d, acc);
         }
 #pragma unroll
@@ -582,6 +625,12 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const int gcol = a.pmap[q0 + j];
     if (gcol >= 0) a.xg[gcol] = xloc[j];
   }
+  {  // shared columns owned by this tile: their final value sits in the last sweep's wrap slot
+    const long long done = ld_relaxed(&a.sync->epoch);
+    const unsigned long long* wrap = a.mbox + (size_t)(done & 1) * a.NB;
+    for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNT)
+      a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + a.lastslot[j], 0ull));
+  }
 }
 
 __global__ void k2_reset(SyncState* sync) {
@@ -621,7 +670,7 @@ struct K2Plan {
   unsigned long long* trace = nullptr;
   int4 *smeta = nullptr, *cmeta = nullptr, *tmeta = nullptr;
   int *tile_slice = nullptr, *tile_chunk = nullptr, *tile_task = nullptr, *pmap_ptr = nullptr, *pmap = nullptr,
-      *lastcol_ptr = nullptr, *lastcol = nullptr, *seed_idx = nullptr, *seed_col = nullptr;
+      *lastcol_ptr = nullptr, *lastcol = nullptr, *lastslot = nullptr, *seed_idx = nullptr, *seed_col = nullptr;
   unsigned long long* mbox = nullptr;
   long long NB = 0;
   int nseed = 0;
@@ -871,7 +920,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
           if (chunk_local >= (1 << 20)) { why = "too many chunks in tile " + std::to_string(t); return false; }
           int mbase = 0;
           if (bnd) {
-            if (NB + (long long)W * R >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
+            if (2 * (NB + (long long)W * R) >= (1LL << 32)) { why = "too many boundary entries for the mailboxes"; return false; }
             mbase = (int)NB;
             for (int r = 0; r < R; r++) {
               mb_of_row[g[a + r]] = NB + r;
@@ -912,8 +961,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   // Random placement costs ~5; here each tile's private columns get residues greedily (most
   // accessed first), each residue chosen to minimise the column's collisions with the residues
   // already in its access groups, under a per-residue capacity; local index = residue + 16 * rank.
+  double bank_stats[3] = {0, 0, 0};
   {
-    std::vector<int32_t> row_of_slice_lane;  // scratch
     pmap.clear();
     for (int t = 0; t < T; t++) {
       const int b = pmap_ptr[t], e = pmap_ptr[t + 1], n = e - b;
@@ -958,6 +1007,18 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
         csize[best]++;
         for (int g : groups_of[x]) cnt[(size_t)g * 16 + best]++;
       }
+      if (getenv("POBK_K2_BANKSTATS")) {  // development aid: modelled wavefronts per x~ access
+        double& acc_new = bank_stats[0]; double& acc_old = bank_stats[1]; double& acc_n = bank_stats[2];
+        std::vector<std::vector<int>> members(ng);
+        for (int x = 0; x < n; x++)
+          for (int g : groups_of[x]) members[g].push_back(x);
+        for (int g = 0; g < ng; g++) {
+          if (members[g].empty()) continue;
+          int a1[16] = {0}, a0[16] = {0}, m1 = 0, m0 = 0;
+          for (int x : members[g]) { m1 = std::max(m1, ++a1[res[x]]); m0 = std::max(m0, ++a0[x & 15]); }
+          acc_new += std::max(m1, 2); acc_old += std::max(m0, 2); acc_n += 1;
+        }
+      }
       int mx = 0;
       for (int k = 0; k < 16; k++) mx = std::max(mx, csize[k]);
       np_t[t] = 16 * mx;
@@ -973,6 +1034,9 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       }
     }
     pmap_ptr[T] = (int)pmap.size();
+    if (bank_stats[2] > 0)
+      fprintf(stderr, "[k2 banks] modelled wavefronts per private x~ access: placed %.2f, unplaced %.2f\n",
+              bank_stats[0] / bank_stats[2], bank_stats[1] / bank_stats[2]);
   }
   const int np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
   const size_t base_smem = fixed + meta_bytes + 16 * ((size_t)np_max + 1);  // + the zero slot
@@ -984,7 +1048,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   // first one's slot of the next sweep and to x~.  mout[row entry] = target slot.
   std::vector<unsigned> mout_of_entry(At.nnz(), 0u);
   std::vector<int> seed_idx, seed_col;
-  std::vector<int> lastcol_ptr(T + 1, 0), lastcol;
+  std::vector<int> lastcol_ptr(T + 1, 0), lastcol, lastslot;
   {
     std::vector<int64_t> cptr(m + 1, 0);
     for (int64_t q = 0; q < At.nnz(); q++) cptr[At.col[q] + 1]++;
@@ -1002,7 +1066,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       const int32_t i = row_of_entry[q];
       return mb_of_row[i] + (q - At.ptr[i]) * R_of_row[i];
     };
-    std::vector<std::vector<int>> per(T);
+    std::vector<std::vector<std::pair<int, int>>> per(T);
     std::vector<int64_t> ch;
     for (int64_t c = 0; c < m; c++) {
       if (!shared[c]) continue;
@@ -1015,11 +1079,11 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       }
       seed_idx.push_back((int)slot_of(ch[0]));
       seed_col.push_back((int)c);
-      per[tile[row_of_entry[ch.back()]]].push_back((int)c);
+      per[tile[row_of_entry[ch.back()]]].push_back({(int)c, (int)slot_of(ch[0])});
     }
     for (int t = 0; t < T; t++) {
       lastcol_ptr[t + 1] = lastcol_ptr[t] + (int)per[t].size();
-      lastcol.insert(lastcol.end(), per[t].begin(), per[t].end());
+      for (auto& pr : per[t]) { lastcol.push_back(pr.first); lastslot.push_back(pr.second); }
     }
   }
 
@@ -1100,6 +1164,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   K2_UP(&k->pmap, pmap.data(), pmap.size());
   K2_UP(&k->lastcol_ptr, lastcol_ptr.data(), lastcol_ptr.size());
   K2_UP(&k->lastcol, lastcol.data(), lastcol.size());
+  K2_UP(&k->lastslot, lastslot.data(), lastslot.size());
   K2_UP(&k->seed_idx, seed_idx.data(), seed_idx.size());
   K2_UP(&k->seed_col, seed_col.data(), seed_col.size());
   K2_UP(&k->mbox, (unsigned long long*)nullptr, 2 * (size_t)std::max<long long>(NB, 1));
@@ -1141,6 +1206,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.pmap = k.pmap;
   a.lastcol_ptr = k.lastcol_ptr;
   a.lastcol = k.lastcol;
+  a.lastslot = k.lastslot;
   a.mbox = k.mbox;
   a.NB = k.NB;
   a.xg = p.d_xt;

@@ -45,16 +45,17 @@ def q(v):
 print("sweep span ns", int(st[:, :, 3].max()))
 task_len, poll, bslice, islice, ready_b, bar_after = [], [], [], [], [], []
 pm, ps, pf, pr = [], [], [], []
+pa, pb, pc, pd = [], [], [], []
 for t in range(T):
     n = tt[t + 1] - tt[t]
     for ti in range(n):
         a = tm[tt[t] + ti]
         nb, ni = a[1] & 0xffff, a[1] >> 16
-        s0, sp, _, s3, r0, d0, r1, d1, m8, m9, m10, _ = st[t, ti]
+        s0, sp, m2, s3, r0, d0, r1, d1, m8, m9, m10, _ = st[t, ti]
         task_len.append(s3 - s0)
         if nb > 0 and sp >= 0:
             poll.append(sp - s0); ready_b.append(r0 - sp); bslice.append(d0 - r0); bar_after.append(s3 - d0)
-            pm.append(m8 - r0); ps.append(sp - m8); pf.append(d0 - sp)
+            pm.append(m8 - r0); ps.append(sp - m8); pf.append(d0 - sp); pa.append(m2 - sp); pb.append(m9 - m2); pc.append(m10 - m9); pd.append(d0 - m10)
         if ni > 0 and r1 >= 0:
             islice.append(d1 - r1)
 print("task (start -> barrier passed)", q(task_len))
@@ -62,6 +63,7 @@ print("  start -> mailboxes full", q(poll))
 print("  first boundary slice: polled->ready", q(ready_b), "compute+publish", q(bslice), "done->barrier", q(bar_after))
 print("  first interior slice compute", q(islice))
 print("  boundary slice: pre", q(pm), " mailbox poll", q(ps), " post (math+stores)", q(pf))
+print("  post: sum", q(pa), " ddiv", q(pb), " pass 2", q(pc), " release", q(pd))
 span = [st[t, tt[t + 1] - tt[t] - 1, 3] - st[t, 0, 0] for t in range(T) if tt[t + 1] > tt[t]]
 print("tile sweep span", q(span))
 t = int(np.argmax([st[t, tt[t + 1] - tt[t] - 1, 3] if tt[t + 1] > tt[t] else -1 for t in range(T)]))
