@@ -72,3 +72,19 @@ for ti in range(tt[t + 1] - tt[t]):
     a = tm[tt[t] + ti]
     print("  task %2d step %2d nb %2d ni %2d | start %7d polled %7d q0 %7d..%7d int %7d..%7d end %7d" %
           ((ti, a[2], a[1] & 0xffff, a[1] >> 16, st[t, ti, 0], st[t, ti, 1], st[t, ti, 4], st[t, ti, 5], st[t, ti, 6], st[t, ti, 7], st[t, ti, 3])))
+
+# per-step fronts: when do tiles finish step k (task end stamp), and how fast does the front move
+ends = {}
+starts = {}
+for t in range(T):
+    for ti in range(tt[t + 1] - tt[t]):
+        k = int(tm[tt[t] + ti][2])
+        ends.setdefault(k, []).append(st[t, ti, 3])
+        starts.setdefault(k, []).append(st[t, ti, 0])
+print("step | tiles | start min/med/max | end min/med/max | end-max delta")
+prev = None
+for k in sorted(ends):
+    e = np.array(ends[k]); s_ = np.array(starts[k])
+    d = (e.max() - prev) if prev is not None else 0
+    prev = e.max()
+    print("%4d | %5d | %7d %7d %7d | %7d %7d %7d | %6d" % (k, len(e), s_.min(), np.median(s_), s_.max(), e.min(), np.median(e), e.max(), d))

@@ -32,7 +32,7 @@ __global__ void mb6(const unsigned char* gblk, int bytes, int R, int W, unsigned
       __syncwarp();
       long long t2 = clock64();
       if (rep == 49 && lane == 0) trp[1] = gtimer();
-      B.post(S, W, xb, mbox_in, mbox + NB, mbox + NB, R, rep == 49 ? trp : nullptr);
+      B.post(S, W, xb, mbox_in, mbox, (unsigned)NB, (unsigned)NB, R, rep == 49 ? trp : nullptr);
       if (rep == 49) { __syncwarp(); if (lane == 0) trp[10] = gtimer(); }
       __syncwarp();
       long long t3 = clock64();
