@@ -19,20 +19,21 @@ __global__ void mb6(const unsigned char* gblk, int bytes, int R, int W, unsigned
   for (int rep = 0; rep < 50; rep++) {
     // refill the mailboxes this slice reads (parity 0)
     for (long long i = lane; i < NB; i += 32) mbox[i] = 0x3FF0000000000000ull;
+    for (int i = lane; i < bytes; i += 32) blk[i] = gblk[i];  // pre() rewrites the slice in place
     __syncwarp();
     __threadfence();
     long long t0 = clock64();
     const SliceAddr S(bs, R, W, mode == 0, lane);
     if (mode == 0) {
       BSlice B;
-      B.pre(S, W, xb);
+      B.pre(S, W, xb, (unsigned)NB, (unsigned)NB);
       long long t1 = clock64();
       unsigned long long* mbox_in = mbox + (lane < R ? lane : 0);
       B.poll(S, W, R, mbox_in);
       __syncwarp();
       long long t2 = clock64();
       if (rep == 49 && lane == 0) trp[1] = gtimer();
-      B.post(S, W, xb, mbox_in, mbox, (unsigned)NB, (unsigned)NB, R, rep == 49 ? trp : nullptr);
+      B.post(S, W, R, mbox, mbox_in, rep == 49 ? trp : nullptr);
       if (rep == 49) { __syncwarp(); if (lane == 0) trp[10] = gtimer(); }
       __syncwarp();
       long long t3 = clock64();
