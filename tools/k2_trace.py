@@ -59,6 +59,9 @@ for t in range(T):
         if ni > 0 and r1 >= 0:
             islice.append(d1 - r1)
 print("task (start -> barrier passed)", q(task_len))
+rb = [st[t, ti, 4] - st[t, ti, 0] for t in range(T) for ti in range(tt[t + 1] - tt[t]) if (tm[tt[t] + ti][1] & 0xffff) > 0 and st[t, ti, 4] >= 0]
+ri = [st[t, ti, 6] - st[t, ti, 0] for t in range(T) for ti in range(tt[t + 1] - tt[t]) if (tm[tt[t] + ti][1] >> 16) > 0 and st[t, ti, 6] >= 0]
+print("  start -> first boundary slice data ready", q(rb), " start -> first interior slice data ready", q(ri))
 print("  start -> mailboxes full", q(poll))
 print("  first boundary slice: polled->ready", q(ready_b), "compute+publish", q(bslice), "done->barrier", q(bar_after))
 print("  first interior slice compute", q(islice))
