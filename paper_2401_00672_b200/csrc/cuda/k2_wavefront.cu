@@ -35,9 +35,9 @@
 //    it owns (its private ones in shared memory, and the shared ones whose last writer in the
 //    sweep it holds, read from the wrap mailbox slot).  Partials are combined in fixed orders;
 //    one grid-wide decision per sweep.
-//  * Warps 0-3 (one per SM sub-partition) take the boundary slices -- the critical path: their
-//    post phases start together when the neighbours' data arrives -- and the other 11 compute
-//    warps the interior slices.
+//  * A task's slices, boundary first, go round-robin over the 15 compute warps, so consecutive
+//    boundary slices (the critical path: their post phases start together when the neighbours'
+//    data arrives) run on different SM sub-partitions.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -59,8 +59,6 @@ constexpr int kNT = 512;            // threads per CTA (one CTA per SM)
 constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
 constexpr int kNC = kNCW * 32;      // compute threads
 constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
-constexpr int kBndWarps = 4;        // warps 0-3 (one per SM sub-partition): boundary slices
-constexpr int kIntWarps = kNCW - kBndWarps;  // the other compute warps: interior slices
 constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
 constexpr int kMinSlots = 4, kMaxSlots = 12;
 constexpr int kSliceRows = 32;      // rows per slice (one lane each)
@@ -514,13 +512,11 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
         unsigned long long* trp = tr ? a.trace + ((size_t)t * a.ntask_max + ti) * 12 : nullptr;
         if (tr && warp == 0 && lane == 0) trp[0] = gtimer();
-        // boundary slices on warps 0-3 (one per sub-partition: their post phases run together when
-        // the neighbours' data arrives), interior ones on the other 11
-        const bool bw = warp < kBndWarps;
-        const int q_first = bw ? warp : nbnd + (warp - kBndWarps);
-        const int q_step = bw ? kBndWarps : kIntWarps, q_end = bw ? nbnd : ntot;
-        for (int q = q_first; q < q_end; q += q_step) {
-          const bool bnd = bw;
+        // the task's slices (boundary first) round-robin over the compute warps: consecutive
+        // boundary slices land on different SM sub-partitions (their post phases run together
+        // when the neighbours' data arrives); large tasks simply take more rounds
+        for (int q = warp; q < ntot; q += kNCW) {
+          const bool bnd = q < nbnd;
           const int4 sl = smeta[tm.x + q];
           const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
           const unsigned long long g = (unsigned long long)sweep * nck + chunk;
