@@ -115,6 +115,8 @@ struct K2Args {
   long long NB;
   double* xg;                 // x~ (RCM frame): x0 in, final out; shared columns' sweep-final values
   const double* xst;          // x~*
+  const double* xsp;          // [pmap size] x~* of the private columns in tile-local order (RSE stop)
+  const double* lcx;          // [lastcol size] x~* of the owned shared columns (RSE stop)
   SyncState* sync;
   double* partials;           // [2*T]
   Ctrl* ctrl;
@@ -438,7 +440,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   int4* cmeta = smeta + a.nsl_max;                           // [nck_max]
   int4* tmeta = cmeta + a.nck_max;                           // [ntask_max]
   double* xloc = (double*)(tmeta + a.ntask_max);             // [np_max + 1] private x~ + the zero slot
-  double* xsloc = xloc + a.np_max + 1;                       // [np_max] private x~* (RSE stop)
 
   const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s0 = a.tile_slice[t], nsl = a.tile_slice[t + 1] - s0;
@@ -465,7 +466,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   for (int j = tid; j < np; j += kNT) {
     const int gcol = a.pmap[q0 + j];  // -1: a hole of the bank-aware placement
     xloc[j] = gcol >= 0 ? a.xg[gcol] : 0.0;
-    xsloc[j] = (rse && gcol >= 0) ? a.xst[gcol] : 0.0;
   }
   __syncthreads();
 
@@ -556,14 +556,22 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         // columns final for this sweep once the tile's last task is done: the private ones, and
         // the shared ones whose last writer (row of the highest step) is in this tile
         double acc = 0.0;
-        for (int j = tid; j < np; j += kNC) {
-          const double d = xloc[j] - xsloc[j];
-          acc = fma(d, d, acc);
+        const double* xsp = a.xsp + q0;  // x~* of the private columns, in local order (0 at holes)
+        for (int j0 = tid; j0 < np; j0 += 8 * kNC) {  // 8 independent loads in flight per thread
+          double xs[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) xs[u] = j0 + u * kNC < np ? __ldg(xsp + j0 + u * kNC) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (j0 + u * kNC < np) {
+              const double d = xloc[j0 + u * kNC] - xs[u];
+              acc = fma(d, d, acc);
+            }
         }
         const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB;  // sweep = sweeps done
         for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNC) {
-          const unsigned long long w = ldm_if(1u, wrap + a.lastslot[j], 0ull);
-          const double d = __longlong_as_double((long long)w) - __ldg(a.xst + a.lastcol[j]);
+          const unsigned long long w = ldm_if(1u, wrap + __ldg(a.lastslot + j), 0ull);
+          const double d = __longlong_as_double((long long)w) - __ldg(a.lcx + j);
           acc = fma(d, d, acc);
         }
 #pragma unroll
@@ -588,11 +596,11 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
           double v = 0.0;
           if (due) {
-            double tot = 0.0;  // tiles in tile order
-            for (int b0 = 0; b0 < a.T; b0 += 32) {
-              const double pv = b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
-              for (int j = 0; j < 32 && b0 + j < a.T; j++) tot += __shfl_sync(kFull, pv, j);
-            }
+            double tot = 0.0;  // fixed order: lane l sums tiles l, l+32, ..., then a fixed butterfly
+            for (int b0 = 0; b0 < a.T; b0 += 32)
+              tot += b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
             v = sqrt(tot) / sqrt(a.ctrl->den);
             if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
             else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
@@ -628,6 +636,20 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const unsigned long long* wrap = a.mbox + (size_t)(done & 1) * a.NB;
     for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNT)
       a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + a.lastslot[j], 0ull));
+  }
+}
+
+// x~* of the private columns in tile-local order (holes: 0) and of the owned shared columns, for
+// the end-of-sweep RSE scan (contiguous per tile: no dependent gathers at the end of a sweep)
+__global__ void k2_gather_xs(int n, const int* __restrict__ pmap, int nl, const int* __restrict__ lastcol,
+                             const double* __restrict__ xst, double* __restrict__ xsp, double* __restrict__ lcx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n + nl; i += gridDim.x * blockDim.x) {
+    if (i < n) {
+      const int c = pmap[i];
+      xsp[i] = c >= 0 ? xst[c] : 0.0;
+    } else {
+      lcx[i - n] = xst[lastcol[i - n]];
+    }
   }
 }
 
@@ -670,6 +692,9 @@ struct K2Plan {
   int *tile_slice = nullptr, *tile_chunk = nullptr, *tile_task = nullptr, *pmap_ptr = nullptr, *pmap = nullptr,
       *lastcol_ptr = nullptr, *lastcol = nullptr, *lastslot = nullptr, *seed_idx = nullptr, *seed_col = nullptr;
   unsigned long long* mbox = nullptr;
+  double* xsp = nullptr;       // [npmap] private x~* in tile-local order
+  double* lcx = nullptr;       // [nlast] owned shared columns' x~*
+  int npmap = 0, nlast = 0;
   long long NB = 0;
   int nseed = 0;
   SyncState* sync = nullptr;
@@ -1037,8 +1062,9 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
               bank_stats[0] / bank_stats[2], bank_stats[1] / bank_stats[2]);
   }
   const int np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
-  const size_t base_smem = fixed + meta_bytes + 16 * ((size_t)np_max + 1);  // + the zero slot
-  const int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
+  const size_t base_smem = fixed + meta_bytes + 8 * ((size_t)np_max + 1);  // private x~ + the zero slot
+  int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
+  if (getenv("POBK_K2_NS_CAP")) NS = std::min(NS, atoi(getenv("POBK_K2_NS_CAP")));  // development experiments
   if (NS < kMinSlots) { why = "shared memory too small for the TMA ring"; return false; }
 
   // the version chain of every shared column c: the rows touching c in schedule (step) order; the
@@ -1131,6 +1157,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   k->np_max = np_max;
   k->smem = (size_t)NS * kSlot + base_smem;
   k->NB = NB;
+  k->npmap = (int)pmap.size();
+  k->nlast = (int)lastcol.size();
   k->nseed = (int)seed_idx.size();
   std::vector<long long> tile_off(T, 0);
   {
@@ -1166,6 +1194,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   K2_UP(&k->seed_idx, seed_idx.data(), seed_idx.size());
   K2_UP(&k->seed_col, seed_col.data(), seed_col.size());
   K2_UP(&k->mbox, (unsigned long long*)nullptr, 2 * (size_t)std::max<long long>(NB, 1));
+  K2_UP(&k->xsp, (double*)nullptr, pmap.size());
+  K2_UP(&k->lcx, (double*)nullptr, lastcol.size());
   K2_UP(&k->orig_q, orig_q.data(), orig_q.size());
   K2_UP(&k->fslot, fslot.data(), fslot.size());
   K2_UP(&k->sync, (SyncState*)nullptr, 1);
@@ -1190,6 +1220,11 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   k2_mbox_seed<<<std::max(1, std::min(148 * 4, (k.nseed + 255) / 256)), 256, 0, s>>>(k.mbox, k.nseed, k.seed_idx, k.seed_col,
                                                                                       p.d_xt);
   launches += 4;
+  if (p.d_xst && k.npmap + k.nlast > 0) {
+    k2_gather_xs<<<std::max(1, std::min(148 * 4, (k.npmap + k.nlast + 255) / 256)), 256, 0, s>>>(
+        k.npmap, k.pmap, k.nlast, k.lastcol, p.d_xst, k.xsp, k.lcx);
+    launches++;
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   K2Args a;
   a.stream = k.stream;
@@ -1209,6 +1244,8 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.NB = k.NB;
   a.xg = p.d_xt;
   a.xst = p.d_xst;
+  a.xsp = k.xsp;
+  a.lcx = k.lcx;
   a.sync = k.sync;
   a.partials = k.partials;
   a.ctrl = p.d_ctrl;
