@@ -113,7 +113,8 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
   for (auto& e : p.ev) CUDA_TRY(cudaEventCreate(&e));
 
   // kernel family: K3 when everything fits one CTA's shared memory, else the K2
-  // wavefront when its tiling is valid, else K1.  Overlapping categories (thr > 0) use K1/K3.
+  // wavefront when its tiling is valid (m >= 4096: measured faster than K1's launch per step
+  // from config 2, 20k rows, upwards), else K1.  Overlapping categories (thr > 0) use K1/K3.
   const int req = p.kernel;
   size_t k3b = 0;
   const bool k3ok = k3_fits(p, k3b);
@@ -126,7 +127,7 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
     if (!k2_build(p, At, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
   } else if (req == POBK_KERNEL_AUTO) {
     if (k3ok) p.kernel = POBK_KERNEL_SMEM;
-    else if (!p.any_overlap && m >= 65536 && k2_build(p, At, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
+    else if (!p.any_overlap && m >= 4096 && k2_build(p, At, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
     else p.kernel = POBK_KERNEL_LAUNCH;
   }
   return POBK_OK;
