@@ -32,9 +32,10 @@
 //    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (warp 15),
 //    which never touches x~.
 //  * The RSE is evaluated at the end of each sweep by each tile over the columns
-//    it owns (its private ones in shared memory, and the shared ones whose last writer in the
-//    sweep it holds, read from the wrap mailbox slot).  Partials are combined in fixed orders;
-//    one grid-wide decision per sweep.
+//    it owns (its private ones, x~ in shared memory, and the shared ones whose last writer in the
+//    sweep it holds, read from the wrap mailbox slot), x~* read from per-tile contiguous arrays
+//    gathered once per solve.  Partials are combined in fixed orders; one grid-wide decision per
+//    sweep.
 //  * A task's slices, boundary first, go round-robin over the 15 compute warps, so consecutive
 //    boundary slices (the critical path: their post phases start together when the neighbours'
 //    data arrives) run on different SM sub-partitions.
@@ -860,7 +861,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
     if (col_tile[c] < 0) col_tile[c] = 0;
   // private columns per tile (ascending), capped so that kMinSlots ring slots still fit
   const size_t fixed = sizeof(Ctl) + 128;
-  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / 16 / 1.04) - 48;  // x~, x~*, zero slot, bank slack
+  // (16 B per column: conservative -- x~ takes 8 -- so that tiles keep a deep TMA ring)
+  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / 16 / 1.04) - 48;
   std::vector<int32_t> local(m, -1);
   std::vector<int> pmap_ptr(T + 1, 0);
   std::vector<int> pmap;
