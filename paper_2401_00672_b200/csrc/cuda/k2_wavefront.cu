@@ -11,12 +11,14 @@
 //     reads the value written by the previous row touching c (in schedule order, wrapping to the
 //     previous sweep) and writes the value read by the next one: each written value has exactly
 //     ONE consumer.  So the writer stores the new x~_c straight into that consumer's MAILBOX slot
-//     (global memory, laid out like the consumer's slice so the consumer's polling loads are
-//     coalesced), and the consumer polls its slots until they no longer hold the sentinel (a
-//     signalling-NaN bit pattern no arithmetic produces), then re-arms them.  8-byte relaxed
-//     accesses are single-copy atomic, so no flags, counters or fences are on the critical path;
-//     slots are double-buffered by sweep parity and the per-sweep grid barrier orders a slot's
-//     re-arm before its next write.
+//     (global memory; a consumer lane's slots are contiguous, entry j at lane*Wp + j with Wp = W
+//     rounded up to 4, so it polls 4 entries per 256-bit load: a global load instruction costs
+//     ~40 cycles of issue whatever its width or its active lanes, measured), and the consumer
+//     polls its slots until they no longer hold the sentinel (a signalling-NaN bit pattern no
+//     arithmetic produces), then re-arms them.  Aligned 8-byte relaxed accesses (also the
+//     elements of a vector access) are single-copy atomic, so no flags, counters or fences are
+//     on the critical path; slots are double-buffered by sweep parity and the per-sweep grid
+//     barrier orders a slot's re-arm before its next write.
 // Results are bitwise those of K1/K3 and of the oracle (the per-row contract of common.cuh).
 //
 //  * Rows are stored as SLICES of <= 32 rows, one lane per row, in ELL order inside the slice
@@ -26,8 +28,9 @@
 //    order) and ||a~_i||^2 is recomputed in registers from the row (the oracle's left-to-right
 //    sum), so a row streams 12 B per stored entry + 10 B (f~, length), and a boundary row another
 //    4 B per entry (the mailbox slot its new value goes to).
-//  * A task's boundary slices come first; their warps load the private operands, then poll the
-//    mailboxes; the interior slices run meanwhile on the other warps.
+//  * A task's boundary slices come first; their warps note the shared entries, poll the
+//    mailboxes, then read the private operands with the row sums; the interior slices run
+//    meanwhile on the other warps.
 //  * The tile's slices are packed, across task boundaries, into <= 16 KB chunks streamed by 1-D
 //    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (warp 15),
 //    which never touches x~.
@@ -203,6 +206,22 @@ __device__ __forceinline__ unsigned lds16(unsigned a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return v;
 }
+// eight shared-memory loads issued back to back (one asm block: the compiler cannot interleave
+// their consumers, so all eight are in flight before the first use)
+__device__ __forceinline__ void lds32x8(unsigned (&v)[8], const unsigned (&a)[8]) {
+  asm volatile(
+      "ld.shared.u32 %0, [%8];\n ld.shared.u32 %1, [%9];\n ld.shared.u32 %2, [%10];\n ld.shared.u32 %3, [%11];\n"
+      " ld.shared.u32 %4, [%12];\n ld.shared.u32 %5, [%13];\n ld.shared.u32 %6, [%14];\n ld.shared.u32 %7, [%15];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+}
+__device__ __forceinline__ void lds64x8(double (&v)[8], const unsigned (&a)[8]) {
+  asm volatile(
+      "ld.shared.f64 %0, [%8];\n ld.shared.f64 %1, [%9];\n ld.shared.f64 %2, [%10];\n ld.shared.f64 %3, [%11];\n"
+      " ld.shared.f64 %4, [%12];\n ld.shared.f64 %5, [%13];\n ld.shared.f64 %6, [%14];\n ld.shared.f64 %7, [%15];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+}
 __device__ __forceinline__ void sts64_if(unsigned p, unsigned a, double v) {
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.shared.f64 [%1], %2;\n}" ::"r"(p), "r"(a), "d"(v)
                : "memory");
@@ -215,6 +234,20 @@ __device__ __forceinline__ unsigned long long ldm_if(unsigned p, const unsigned 
                : "r"(p), "l"(a)
                : "memory");
   return v;
+}
+// four consecutive mailbox words of one lane (32-byte aligned), one 256-bit load: each word is
+// still an aligned 8-byte single-copy-atomic access; unchanged registers when p == 0
+__device__ __forceinline__ void ldm4_if(unsigned p, const unsigned long long* a, double& x0, double& x1, double& x2,
+                                        double& x3) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n @q ld.relaxed.gpu.global.v4.b64 {%0, %1, %2, %3}, [%5];\n}"
+               : "+d"(x0), "+d"(x1), "+d"(x2), "+d"(x3)
+               : "r"(p), "l"(a)
+               : "memory");
+}
+__device__ __forceinline__ void stm4_if(unsigned p, unsigned long long* a, unsigned long long v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.v4.b64 [%1], {%2, %2, %2, %2};\n}" ::"r"(p),
+               "l"(a), "l"(v)
+               : "memory");
 }
 __device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsigned long long v) {
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a),
@@ -284,10 +317,12 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
   }
 }
 
-// boundary slice, in two halves: pre() loads the PRIVATE x~ (final for this step as soon as the
-// tile's previous task is done) and notes the shared entries; post() polls the shared entries'
-// mailboxes (this lane's slot of entry j: mbox_in + j*R), re-arms them, applies the rows, writes
-// private results to shared memory and shared results to their consumers' mailboxes.  (A sweep's
+// boundary slice: pre() notes the shared entries; poll() loads the shared entries' mailboxes
+// (this lane's slots are contiguous, entry j at mbox_in + j: one 256-bit load per 4 entries -- a
+// global load instruction costs ~40 cycles of issue whatever its width or active lanes) until no
+// sentinel is left, then re-arms them; post() reads the PRIVATE x~ (final for this step once the
+// tile's previous task is done) while it forms the row sums, applies the rows, writes private
+// results to shared memory and shared results to their consumers' mailboxes.  (A sweep's
 // last writer of a column writes the next sweep's first reader's slot, which therefore holds the
 // column's sweep-final value until that reader runs: the RSE and the final write-back read it.)
 struct BSlice {
@@ -303,29 +338,22 @@ struct BSlice {
         for (int u = 0; u < kBatch; u++) cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {
-          const unsigned c = cr[u];
-          const bool sh = (c & kShared) && jb + u < S.myl;
+          const bool sh = (cr[u] & kShared) && jb + u < S.myl;
           shm |= sh ? (1u << (jb + u)) : 0u;
-          xr[jb + u] = ((c & kShared) || jb + u >= W) ? 0.0 : lds64(xb + 8u * c);
         }
       }
     }
   }
   // poll this lane's shared entries j < kMaxJ until every lane of the warp has all of them
-  __device__ __forceinline__ void poll(const SliceAddr& S, int W, int R, unsigned long long* mbox_in) {
+  __device__ __forceinline__ void poll(const SliceAddr& S, int W, int R, unsigned long long* mbox_in,
+                                       unsigned long long* trp = nullptr) {
     unsigned pend = shm;
+    int it = 0;
     while (true) {
+      it++;
 #pragma unroll
-      for (int jb = 0; jb < kMaxJ; jb += kBatch) {
-        if (jb < W) {
-#pragma unroll
-          for (int u = 0; u < kBatch; u++) {
-            const unsigned long long w =
-                ldm_if((pend >> (jb + u)) & 1u, mbox_in + (size_t)(jb + u) * R, (unsigned long long)__double_as_longlong(xr[jb + u]));
-            xr[jb + u] = __longlong_as_double((long long)w);
-          }
-        }
-      }
+      for (int j4 = 0; j4 < kMaxJ; j4 += 4)  // (the other entries of a group: overwritten in post)
+        if (j4 < W) ldm4_if((pend >> j4) & 0xFu, mbox_in + j4, xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3]);
       unsigned np = 0u;
 #pragma unroll
       for (int j = 0; j < kMaxJ; j++)
@@ -333,9 +361,11 @@ struct BSlice {
       pend = np;
       if (!__any_sync(kFull, pend != 0u)) break;
     }
+    if (trp && (threadIdx.x & 31) == 0) trp[11] = (unsigned long long)it;
     // re-arm the consumed slots for the sweep after next (ordered by the per-sweep grid barrier)
 #pragma unroll
-    for (int j = 0; j < kMaxJ; j++) stm_if((shm >> j) & 1u, mbox_in + (size_t)j * R, kSentinel);
+    for (int j4 = 0; j4 < kMaxJ; j4 += 4)
+      if (j4 < W) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
@@ -345,11 +375,27 @@ struct BSlice {
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
       if (jb < W) {
-        double av[kBatch];
+        // a batch: columns, then the private x~ (always a valid address: branch-free), then the
+        // values -- all loads in flight before the first use
+        static_assert(kBatch == 8, "batched loads are written for 8");
+        double av[kBatch], xp[kBatch];
+        unsigned cr[kBatch], ad[kBatch];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) av[u] = jb + u < W ? lds64(S.vb + min(jb + u, W - 1) * S.vs) : 0.0;
+        for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
+        lds32x8(cr, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = xb + 8u * ((cr[u] & kShared) ? 0u : cr[u]);
+        lds64x8(xp, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
+        lds64x8(av, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) av[u] = jb + u < W ? av[u] : 0.0;
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {  // past the width: +0 * +0 (xr, av are +0 there)
+          const int j = jb + u;
+          const bool priv = j < W && !(cr[u] & kShared);
+          xr[j] = ((shm >> j) & 1u) ? xr[j] : (priv ? xp[u] : 0.0);
           s = __dadd_rn(s, __dmul_rn(av[u], xr[jb + u]));
           n2 = __dadd_rn(n2, __dmul_rn(av[u], av[u]));
         }
@@ -362,7 +408,7 @@ struct BSlice {
       if ((cj & kShared) && j < S.myl) {
         unsigned long long w;
         do {
-          w = ldm_if(1u, mbox_in + (size_t)j * R, 0ull);
+          w = ldm_if(1u, mbox_in + j, 0ull);
         } while (w == kSentinel);  // (re-armed in pass 2, after it is read again)
         x = __longlong_as_double((long long)w);
       } else if (!(cj & kShared)) {
@@ -417,8 +463,8 @@ struct BSlice {
       const unsigned cj = lds32(S.cb + j * S.cs), idx = cj & kIdx;
       const double a = lds64(S.vb + j * S.vs);
       if ((cj & kShared) && j < S.myl) {
-        const unsigned long long w = ldm_if(1u, mbox_in + (size_t)j * R, 0ull);
-        stm_if(1u, mbox_in + (size_t)j * R, kSentinel);
+        const unsigned long long w = ldm_if(1u, mbox_in + j, 0ull);
+        stm_if(1u, mbox_in + j, kSentinel);
         {
           const double x1 = __dadd_rn(__longlong_as_double((long long)w), __dmul_rn(alpha, a));
           const unsigned mo = lds32(S.mb + j * S.cs);
@@ -531,8 +577,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             BSlice B;
             B.pre(S, W, xb);
             if (tr && q == 0 && lane == 0) trp[8] = gtimer();
-            unsigned long long* const mbox_in = mbox_p + sl.w + (lane < R ? lane : 0);
-            B.poll(S, W, R, mbox_in);
+            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
+            B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
             if (tr && q == 0 && lane == 0) trp[1] = gtimer();
             B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
             if (tr && q == 0) {
@@ -913,7 +959,6 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   std::vector<int64_t> slice_pos;                // byte offset of each slice in the stream
   std::vector<uint8_t> slice_bnd;
   std::vector<int64_t> mb_of_row(m, -1);         // boundary rows: mailbox index of entry 0
-  std::vector<int32_t> R_of_row(m, 0);
   long long off = 0, pad = 0, NB = 0;
   int nsl_max = 1, nck_max = 1, ntask_max = 1;
   for (int t = 0; t < T; t++) {
@@ -945,13 +990,11 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
           if (chunk_local >= (1 << 20)) { why = "too many chunks in tile " + std::to_string(t); return false; }
           int mbase = 0;
           if (bnd) {
-            if (2 * (NB + (long long)W * R) >= (1LL << 32)) { why = "too many boundary entries for the mailboxes"; return false; }
+            const int Wp = (W + 3) & ~3;  // a lane's slots: contiguous, 32-byte aligned groups of 4
+            if (2 * (NB + (long long)Wp * R) >= (1LL << 32)) { why = "too many boundary entries for the mailboxes"; return false; }
             mbase = (int)NB;
-            for (int r = 0; r < R; r++) {
-              mb_of_row[g[a + r]] = NB + r;
-              R_of_row[g[a + r]] = R;
-            }
-            NB += (long long)W * R;
+            for (int r = 0; r < R; r++) mb_of_row[g[a + r]] = NB + (long long)r * Wp;
+            NB += (long long)Wp * R;
           }
           smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W, mbase));
           slice_rows.emplace_back(g.begin() + a, g.begin() + b);
@@ -1090,7 +1133,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) row_of_entry[q] = (int32_t)i;
     auto slot_of = [&](int64_t q) {  // mailbox slot of CSR entry q (its row is a boundary row)
       const int32_t i = row_of_entry[q];
-      return mb_of_row[i] + (q - At.ptr[i]) * R_of_row[i];
+      return mb_of_row[i] + (q - At.ptr[i]);
     };
     std::vector<std::vector<std::pair<int, int>>> per(T);
     std::vector<int64_t> ch;

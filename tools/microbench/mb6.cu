@@ -26,14 +26,14 @@ __global__ void mb6(const unsigned char* gblk, int bytes, int R, int W, unsigned
     const SliceAddr S(bs, R, W, mode == 0, lane);
     if (mode == 0) {
       BSlice B;
-      B.pre(S, W, xb, (unsigned)NB, (unsigned)NB);
+      B.pre(S, W, xb);
       long long t1 = clock64();
-      unsigned long long* mbox_in = mbox + (lane < R ? lane : 0);
+      unsigned long long* mbox_in = mbox + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
       B.poll(S, W, R, mbox_in);
       __syncwarp();
       long long t2 = clock64();
       if (rep == 49 && lane == 0) trp[1] = gtimer();
-      B.post(S, W, R, mbox, mbox_in, rep == 49 ? trp : nullptr);
+      B.post(S, W, xb, mbox_in, mbox, (unsigned)NB, (unsigned)NB, R, rep == 49 ? trp : nullptr);
       if (rep == 49) { __syncwarp(); if (lane == 0) trp[10] = gtimer(); }
       __syncwarp();
       long long t3 = clock64();
@@ -73,7 +73,7 @@ int main() {
           val[e] = 0.5 + (rng() % 1000) * 1e-3;
           const bool sh = bnd && (rng() % 2 == 0);
           col[e] = sh ? (0x80000000u | (unsigned)(rng() % 100000)) : (unsigned)(rng() % 8192);
-          if (bnd) mout[e] = sh ? (unsigned)(rng() % (W * R)) : 0u;
+          if (bnd) mout[e] = sh ? (unsigned)(rng() % (((W + 3) & ~3) * R)) : 0u;
         } else {
           col[e] = 8192;  // zero slot
         }
@@ -85,12 +85,12 @@ int main() {
     unsigned long long* trp;
     cudaMalloc(&trp, 16 * 8);
     cudaMalloc(&d, h.size());
-    cudaMalloc(&mb, 2 * W * R * 8);
+    cudaMalloc(&mb, 2 * ((W + 3) & ~3) * R * 8);
     cudaMalloc(&out, 32);
     cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice);
     const size_t sm = ((h.size() + 127) & ~127) + 8193 * 8;
     cudaFuncSetAttribute(mb6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    mb6<<<1, 128, sm>>>(d, (int)h.size(), R, W, mb, W * R, out, mode, trp);
+    mb6<<<1, 128, sm>>>(d, (int)h.size(), R, W, mb, ((W + 3) & ~3) * R, out, mode, trp);
     cudaError_t e = cudaDeviceSynchronize();
     long long o[4];
     cudaMemcpy(o, out, 32, cudaMemcpyDeviceToHost);
