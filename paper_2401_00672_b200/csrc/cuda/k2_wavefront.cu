@@ -59,11 +59,15 @@
 namespace pobk {
 
 namespace {
-constexpr int kNT = 512;            // threads per CTA (one CTA per SM)
+#ifndef POBK_K2_NT
+#define POBK_K2_NT 256
+#endif
+constexpr int kNT = POBK_K2_NT;     // threads per CTA (one CTA per SM)
 constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
 constexpr int kNC = kNCW * 32;      // compute threads
 constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
 constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
+static_assert(kSlot <= 65536, "slice offsets are packed in 16 bits");
 constexpr int kMinSlots = 4, kMaxSlots = 12;
 constexpr int kSliceRows = 32;      // rows per slice (one lane each)
 #ifndef POBK_K2_MAXJ
@@ -104,7 +108,7 @@ struct SyncState {
 struct K2Args {
   const unsigned char* stream;
   const long long* tile_off;  // [T] byte offset of each tile's first chunk
-  const int4* smeta;          // slices: {chunk | R << 20, offset in chunk, W, mailbox base (boundary)}
+  const int4* smeta;          // slices: {chunk | R << 20, offset in chunk | (chunk mod 2NS) << 16, W, mailbox base (boundary)}
   const int* tile_slice;      // [T+1]
   const int4* cmeta;          // chunks: {offset from tile base, bytes, slices, 0}
   const int* tile_chunk;      // [T+1]
@@ -170,9 +174,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+// POBK_K2_FT (development): trace stamps in SM clock cycles instead of global nanoseconds, plus
+// stamps inside the boundary post (tools/k2_ft.py)
+#ifndef POBK_K2_FT
+#define POBK_K2_FT 0
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long v;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  if (POBK_K2_FT)
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(v));
+  else
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
   return v;
 }
 __device__ __forceinline__ int ld_vol_shared(const int* p) { return *(const volatile int*)p; }
@@ -182,6 +194,33 @@ __device__ __forceinline__ unsigned long long ld_vol_shared64(const unsigned lon
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// Boundary priority (POBK_K2_PRIO): after the barrier that closes task k-1, the interior warps
+// wait (named barrier 3) until the look-ahead boundary warps -- the critical path to the
+// neighbouring tiles -- have read their operands (1: after the whole post, 2: after the row sums),
+// so that their shared-memory traffic does not queue behind the interior slices'.
+#ifndef POBK_K2_PRIO
+#define POBK_K2_PRIO 0
+#endif
+constexpr int kPrio = POBK_K2_PRIO;
+// Development ablations (wrong numerics; timing only): bit 0 no mailbox wait, bit 1 no per-task
+// barrier, bit 2 interior slices skipped, bit 3 boundary post skipped, bit 4 every slice skipped,
+// bit 5 no private stores in the boundary write-back, bit 6 weak mailbox stores, bit 7 no re-arm.
+#ifndef POBK_K2_PSLEEP
+#define POBK_K2_PSLEEP 64  // producer back-off while its next ring slot is still in use (ns)
+#endif
+#ifndef POBK_K2_CSLEEP
+#define POBK_K2_CSLEEP 32  // consumer back-off while its chunk is not issued yet (ns)
+#endif
+#ifndef POBK_K2_POLLSLEEP
+#define POBK_K2_POLLSLEEP 0  // back-off between mailbox poll rounds (ns)
+#endif
+#ifndef POBK_K2_ABL
+#define POBK_K2_ABL 0
+#endif
+constexpr int kAbl = POBK_K2_ABL;
 
 // ------------------------------------------------------------------ slice arithmetic
 // All shared-memory operands are addressed through 32-bit shared-window addresses held in
@@ -250,6 +289,10 @@ __device__ __forceinline__ void stm4_if(unsigned p, unsigned long long* a, unsig
                : "memory");
 }
 __device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsigned long long v) {
+  if (POBK_K2_ABL & 64) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a), "l"(v) : "memory");
+    return;
+  }
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a),
                "l"(v)
                : "memory");
@@ -280,8 +323,80 @@ struct SliceAddr {
 
 // interior slice: every column private (shared memory at xb); pass 2 re-reads x~ from shared
 // memory (unchanged in between: no other row of the category touches these columns)
+#ifndef POBK_K2_ICACHE
+#define POBK_K2_ICACHE 0
+#endif
+constexpr int kICache = POBK_K2_ICACHE;  // interior entries kept in registers between the passes
 __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsigned xb) {
   double s = 0.0, n2 = 0.0;
+  if constexpr (kICache > 0) {
+    // entries j < kICache: column, x~ and value stay in registers for pass 2 (x~ is unchanged in
+    // between: no other row of the category touches these columns)
+    constexpr int kIC = kICache > 0 ? kICache : 1;
+    unsigned cc[kIC];
+    double cx[kIC], ca[kIC];
+#pragma unroll
+    for (int jb = 0; jb < kICache; jb += kBatch) {
+      if (jb < W) {
+        unsigned ad[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
+        unsigned c8[kBatch];
+        lds32x8(c8, ad);
+        double x8[kBatch], a8[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = xb + 8u * c8[u];
+        lds64x8(x8, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
+        lds64x8(a8, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const bool in = jb + u < W;
+          cc[jb + u] = c8[u];
+          ca[jb + u] = in ? a8[u] : 0.0;
+          cx[jb + u] = in ? x8[u] : 0.0;
+          s = __dadd_rn(s, __dmul_rn(ca[jb + u], cx[jb + u]));
+          n2 = __dadd_rn(n2, __dmul_rn(ca[jb + u], ca[jb + u]));
+        }
+      }
+    }
+    for (int jb = kICache; jb < W; jb += kBatch) {
+      unsigned c[kBatch];
+      double av[kBatch], xv[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        const bool in = jb + u < W;
+        const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
+        s = __dadd_rn(s, __dmul_rn(a, x));
+        n2 = __dadd_rn(n2, __dmul_rn(a, a));
+      }
+    }
+    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+#pragma unroll
+    for (int j = 0; j < kICache; j++)
+      if (j < W) sts64_if(j < S.myl, xb + 8u * cc[j], __dadd_rn(cx[j], __dmul_rn(alpha, ca[j])));
+    for (int jb = kICache; jb < W; jb += kBatch) {
+      unsigned c[kBatch];
+      double av[kBatch], xv[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+        av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
+    }
+    return;
+  }
   for (int jb = 0; jb < W; jb += kBatch) {
     unsigned c[kBatch];
     double av[kBatch], xv[kBatch];
@@ -359,18 +474,19 @@ struct BSlice {
       for (int j = 0; j < kMaxJ; j++)
         if ((pend >> j) & 1u) np |= ((unsigned long long)__double_as_longlong(xr[j]) == kSentinel) ? (1u << j) : 0u;
       pend = np;
+      if (kAbl & 1) break;
       if (!__any_sync(kFull, pend != 0u)) break;
     }
     if (trp && (threadIdx.x & 31) == 0) trp[11] = (unsigned long long)it;
     // re-arm the consumed slots for the sweep after next (ordered by the per-sweep grid barrier)
 #pragma unroll
     for (int j4 = 0; j4 < kMaxJ; j4 += 4)
-      if (j4 < W) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
+      if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
                                        unsigned long long* mbox, unsigned off_p, unsigned off_q, int R,
-                                       unsigned long long* trp) {
+                                       unsigned long long* trp, bool arrive) {
     double s = 0.0, n2 = 0.0;
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
@@ -417,6 +533,11 @@ struct BSlice {
       s = __dadd_rn(s, __dmul_rn(a, x));
       n2 = __dadd_rn(n2, __dmul_rn(a, a));
     }
+    if (kPrio == 2 && arrive) {
+      double s2 = s;
+      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
+      named_arrive(3, kNC);
+    }
     if (trp) {
       double s2 = s;
       asm volatile("mov.b64 %0, %0;" : "+d"(s2));
@@ -440,6 +561,11 @@ struct BSlice {
         for (int u = 0; u < kBatch; u++) xr[jb + u] = __dadd_rn(xr[jb + u], __dmul_rn(alpha, av[u]));
       }
     }
+    if (POBK_K2_FT && trp) {
+      double a2 = xr[0];
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
+    }
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // write back: a batch of mailbox targets, then its stores
       if (jb < W) {
@@ -453,7 +579,7 @@ struct BSlice {
         for (int u = 0; u < kBatch; u++) {
           const int j = jb + u;
           const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
-          sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
+          if (!(kAbl & 32)) sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
           stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
                  (unsigned long long)__double_as_longlong(xr[j]));
         }
@@ -475,8 +601,190 @@ struct BSlice {
         sts64_if(1u, ca, __dadd_rn(lds64(ca), __dmul_rn(alpha, a)));
       }
     }
+    if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
+
+// four predicated shared-memory loads in one asm block (registers keep their value where the
+// predicate is off)
+__device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, double& v3, unsigned p0, unsigned p1,
+                                           unsigned p2, unsigned p3, unsigned a0, unsigned a1, unsigned a2, unsigned a3) {
+  asm volatile(
+      "{\n .reg .pred q0, q1, q2, q3;\n setp.ne.u32 q0, %4, 0;\n setp.ne.u32 q1, %5, 0;\n setp.ne.u32 q2, %6, 0;\n"
+      " setp.ne.u32 q3, %7, 0;\n @q0 ld.shared.f64 %0, [%8];\n @q1 ld.shared.f64 %1, [%9];\n"
+      " @q2 ld.shared.f64 %2, [%10];\n @q3 ld.shared.f64 %3, [%11];\n}"
+      : "+d"(v0), "+d"(v1), "+d"(v2), "+d"(v3)
+      : "r"(p0), "r"(p1), "r"(p2), "r"(p3), "r"(a0), "r"(a1), "r"(a2), "r"(a3));
+}
+
+// Register-resident boundary slice (POBK_K2_BREG, default): the row's columns, values and
+// ||a~||^2 are loaded from the ring BEFORE the barrier that closes the tile's previous task,
+// together with the mailbox poll; after the barrier only the private x~ loads (all in flight at
+// once), the row sum, the division and the write-back remain on the critical path.  Same
+// arithmetic in the same order as BSlice (the common.cuh contract).
+struct BSlice2 {
+  double xr[kMaxJ];
+  double av[kMaxJ];
+  unsigned cr[kMaxJ];
+  unsigned shm;
+  double n2;
+  __device__ __forceinline__ void pre(const SliceAddr& S, int W) {
+    shm = 0u;
+    n2 = 0.0;
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+      if (jb < W) {
+        unsigned ad[kBatch], c8[kBatch];
+        double a8[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
+        lds32x8(c8, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
+        lds64x8(a8, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const int j = jb + u;
+          cr[j] = c8[u];
+          av[j] = j < W ? a8[u] : 0.0;
+          const bool sh = (c8[u] & kShared) && j < S.myl;
+          shm |= sh ? (1u << j) : 0u;
+          n2 = __dadd_rn(n2, __dmul_rn(av[j], av[j]));  // left to right, as the oracle
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void poll(int W, unsigned long long* mbox_in) {
+    unsigned pend = shm;
+    while (true) {
+#pragma unroll
+      for (int j4 = 0; j4 < kMaxJ; j4 += 4)
+        if (j4 < W) ldm4_if((pend >> j4) & 0xFu, mbox_in + j4, xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3]);
+      unsigned np = 0u;
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j++)
+        if ((pend >> j) & 1u) np |= ((unsigned long long)__double_as_longlong(xr[j]) == kSentinel) ? (1u << j) : 0u;
+      pend = np;
+      if (kAbl & 1) {  // ablation: no wait (an empty slot reads as +0, not as the NaN sentinel)
+#pragma unroll
+        for (int j = 0; j < kMaxJ; j++)
+          if ((pend >> j) & 1u) xr[j] = 0.0;
+        break;
+      }
+      if (!__any_sync(kFull, pend != 0u)) break;
+      if (POBK_K2_POLLSLEEP) __nanosleep(POBK_K2_POLLSLEEP);
+    }
+#pragma unroll
+    for (int j4 = 0; j4 < kMaxJ; j4 += 4)
+      if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
+  }
+  __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
+                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
+                                       bool arrive) {
+    // private x~ of entries j < W (final once the tile's previous task is done): all loads in
+    // flight before the first use; shared entries keep the polled value; entries >= W are +0
+#pragma unroll
+    for (int j = 0; j < kMaxJ; j++)
+      if ((j & ~(kBatch - 1)) < W) xr[j] = ((shm >> j) & 1u) ? xr[j] : 0.0;
+#pragma unroll
+    for (int j4 = 0; j4 < kMaxJ; j4 += 4) {
+      if (j4 < W) {
+        unsigned p[4], ad[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          p[u] = (j4 + u < W && !(cr[j4 + u] & kShared)) ? 1u : 0u;
+          ad[u] = xb + 8u * (cr[j4 + u] & kIdx);
+        }
+        lds64x4_if(xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3], p[0], p[1], p[2], p[3], ad[0], ad[1], ad[2], ad[3]);
+      }
+    }
+    if (POBK_K2_FT && trp) {  // all private x~ loads complete
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[j]));
+      if ((threadIdx.x & 31) == 0) trp[11] = gtimer();
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxJ; j++)
+      if ((j & ~(kBatch - 1)) < W) s = __dadd_rn(s, __dmul_rn(av[j], xr[j]));
+    double n2t = n2;
+    for (int j = kMaxJ; j < W; j++) {  // long rows: entries past the register window
+      const unsigned cj = lds32(S.cb + j * S.cs);
+      const double a = lds64(S.vb + j * S.vs);
+      double x = 0.0;
+      if ((cj & kShared) && j < S.myl) {
+        unsigned long long w;
+        do {
+          w = ldm_if(1u, mbox_in + j, 0ull);
+        } while (w == kSentinel);  // (re-armed in the write-back, after it is read again)
+        x = __longlong_as_double((long long)w);
+      } else if (!(cj & kShared)) {
+        x = lds64(xb + 8u * (cj & kIdx));
+      }
+      s = __dadd_rn(s, __dmul_rn(a, x));
+      n2t = __dadd_rn(n2t, __dmul_rn(a, a));
+    }
+    if (kPrio == 2 && arrive) {
+      double s2 = s;
+      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
+      named_arrive(3, kNC);
+    }
+    if (trp) {
+      double s2 = s;
+      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
+    }
+    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2t);
+    if (trp) {
+      double a2 = alpha;
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[9] = gtimer();
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxJ; j++) xr[j] = __dadd_rn(xr[j], __dmul_rn(alpha, av[j]));
+    if (POBK_K2_FT && trp) {
+      double a2 = xr[0];
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
+    }
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // write back: a batch of mailbox targets, then its stores
+      if (jb < W) {
+        unsigned mo[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) mo[u] = lds32(S.mb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const int j = jb + u;
+          const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
+          if (!(kAbl & 32)) sts64_if(act & (sh ^ 1u), xb + 8u * (cr[j] & kIdx), xr[j]);
+          stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
+                 (unsigned long long)__double_as_longlong(xr[j]));
+        }
+      }
+    }
+    for (int j = kMaxJ; j < W; j++) {  // tail: the slot still holds the consumed value (re-armed now)
+      const unsigned cj = lds32(S.cb + j * S.cs), idx = cj & kIdx;
+      const double a = lds64(S.vb + j * S.vs);
+      if ((cj & kShared) && j < S.myl) {
+        const unsigned long long w = ldm_if(1u, mbox_in + j, 0ull);
+        stm_if(1u, mbox_in + j, kSentinel);
+        const double x1 = __dadd_rn(__longlong_as_double((long long)w), __dmul_rn(alpha, a));
+        const unsigned mo = lds32(S.mb + j * S.cs);
+        stm_if(1u, mbox + ((mo & ~kWrap) + ((mo & kWrap) ? off_q : off_p)), (unsigned long long)__double_as_longlong(x1));
+      } else if (!(cj & kShared) && j < S.myl) {
+        const unsigned ca = xb + 8u * idx;
+        sts64_if(1u, ca, __dadd_rn(lds64(ca), __dmul_rn(alpha, a)));
+      }
+    }
+    if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
+  }
+};
+#ifndef POBK_K2_BREG
+#define POBK_K2_BREG 1
+#endif
 
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -528,7 +836,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       int slot = 0, c = 0;
       while (!ld_vol_shared(&ctl->stop)) {
         if (g >= gmax || (g >= (unsigned long long)NS && ld_vol_shared(&ctl->released[slot]) < cum[slot])) {
-          __nanosleep(64);
+          if (POBK_K2_PSLEEP) __nanosleep(POBK_K2_PSLEEP);
           continue;
         }
         const int4 cm = cmeta[c];
@@ -550,52 +858,95 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const unsigned xb = opaque(smem_u32(xloc));
     const unsigned ring_s = opaque(smem_u32(ring));
     long long sweep = 0;
+    const int nck2 = nck % (2 * NS);
+    int hbase = 0;  // (sweep * nck) mod 2NS
     while (sweep < maxs) {
       const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
+      int rot = 0;  // continuous round-robin: slice q of task ti runs on warp (rot_ti + q) mod kNCW
       for (int ti = 0; ti < ntask; ti++) {
         const int4 tm = tmeta[ti];
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
         unsigned long long* trp = tr ? a.trace + ((size_t)t * a.ntask_max + ti) * 12 : nullptr;
-        if (tr && warp == 0 && lane == 0) trp[0] = gtimer();
+        // this warp's first slice of the task; the slices of consecutive tasks continue the
+        // round-robin where the previous task stopped, so task ti's boundary slices land on warps
+        // that are not busy with task ti-1's (their look-ahead overlaps the previous post)
+        const int qw = warp >= rot ? warp - rot : warp - rot + kNCW;
+        rot += ntot % kNCW;
+        rot = rot >= kNCW ? rot - kNCW : rot;
+        if (tr && qw == 0 && lane == 0) trp[0] = gtimer();
+        // LOOK-AHEAD: this warp's first boundary slice of task ti (q = qw).  Its operands and the
+        // neighbours' values (mailboxes) do not depend on the tile's task ti-1, so they are fetched
+        // and awaited BEFORE the barrier that closes task ti-1; only the private x~ reads (post)
+        // come after it.  (No deadlock: every slice of task ti-1 this warp owns is done, and the
+        // producers of task ti's inputs are rows of earlier steps.)  The slice's chunk must not wait
+        // for a ring slot that a slice of task ti frees: chunk g is issued once chunk g - NS is
+        // consumed, so it has to lie within NS chunks of the task's first one.
+        const int4 sl0 = smeta[tm.x + (qw < nbnd ? qw : 0)];
+        const bool la = qw < nbnd && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
+        if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
+        if (kPrio && !la) named_bar(3, kNC);    // boundary priority
         // the task's slices (boundary first) round-robin over the compute warps: consecutive
         // boundary slices land on different SM sub-partitions (their post phases run together
         // when the neighbours' data arrives); large tasks simply take more rounds
-        for (int q = warp; q < ntot; q += kNCW) {
+        for (int q = qw; q < ntot; q += kNCW) {
           const bool bnd = q < nbnd;
           const int4 sl = smeta[tm.x + q];
           const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
           const unsigned long long g = (unsigned long long)sweep * nck + chunk;
-          const int slot = (int)(g % (unsigned)NS);
-          while (ld_vol_shared64(&ctl->issued) <= g) __nanosleep(32);  // ring full: let the others use the smem pipe
-          mbar_wait(&ctl->full[slot], (unsigned)((g / (unsigned)NS) & 1));
-          const unsigned blk = ring_s + (unsigned)(slot * kSlot + sl.y);
-          if (tr && lane == 0 && (q == 0 || q == nbnd)) trp[q == 0 ? 4 : 6] = gtimer();
+          // ring position of chunk g without 64-bit division: h = g mod 2NS from the sweep's base
+          // and the chunk's residue (precomputed); slot = h mod NS, phase parity = h >= NS
+          int h = hbase + (sl.y >> 16);
+          h = h >= 2 * NS ? h - 2 * NS : h;
+          const int slot = h >= NS ? h - NS : h;
+          while (ld_vol_shared64(&ctl->issued) <= g)  // ring full: let the others use the smem pipe
+            if (POBK_K2_CSLEEP) __nanosleep(POBK_K2_CSLEEP);
+          mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
+          const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
+          if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
           const SliceAddr S(blk, R, W, bnd, lane);
-          if (bnd) {
+          if (kAbl & 16) {
+            if (la && q == qw && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
+          } else if (bnd) {
+#if POBK_K2_BREG
+            BSlice2 B;
+            B.pre(S, W);
+            if (tr && q == 0 && lane == 0) trp[8] = gtimer();
+            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
+            B.poll(W, mbox_in);
+#else
             BSlice B;
             B.pre(S, W, xb);
             if (tr && q == 0 && lane == 0) trp[8] = gtimer();
             unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
             B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
+#endif
             if (tr && q == 0 && lane == 0) trp[1] = gtimer();
-            B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
+            if (la && q == qw && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // look-ahead slice: task ti-1 now complete
+            if (tr && q == 0 && lane == 0) trp[3] = gtimer();
+#if POBK_K2_BREG
+            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, la && q == qw);
+#else
+            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr, la && q == qw);
+#endif
+            if (kPrio == 1 && la && q == qw) named_arrive(3, kNC);
             if (tr && q == 0) {
               __syncwarp();
               if (lane == 0) trp[10] = gtimer();
             }
-          } else {
+          } else if (!(kAbl & 4)) {
             slice_interior(S, W, xb);
           }
           __syncwarp();
           if (lane == 0) atomicAdd(&ctl->released[slot], 1);
-          if (tr && lane == 0 && (q == 0 || q == nbnd)) trp[q == 0 ? 5 : 7] = gtimer();
+          if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 5 : 7] = gtimer();
         }
-        named_bar(1, kNC);  // task k before task k+1 inside the tile
-        if (tr && warp == 0 && lane == 0) trp[3] = gtimer();
       }
+      named_bar(1, kNC);  // the sweep's last task is complete
       sweep++;
+      hbase += nck2;
+      hbase = hbase >= 2 * NS ? hbase - 2 * NS : hbase;
       // ---- end of sweep: a grid barrier every sweep (it also orders the mailbox re-arms of this
       //      sweep before the writes of the next ones); the stop test when due
       const bool due = mode == POBK_STOP_RSE && ((sweep % every) == 0 || sweep >= maxs);
@@ -1111,6 +1462,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
   if (getenv("POBK_K2_NS_CAP")) NS = std::min(NS, atoi(getenv("POBK_K2_NS_CAP")));  // development experiments
   if (NS < kMinSlots) { why = "shared memory too small for the TMA ring"; return false; }
+  // slice meta .y = offset in chunk (< 2^16) | (tile-local chunk index mod 2NS) << 16
+  for (auto& sm : smeta) sm.y |= ((sm.x & 0xfffff) % (2 * NS)) << 16;
 
   // the version chain of every shared column c: the rows touching c in schedule (step) order; the
   // value written by the p-th goes to the (p+1)-th's mailbox slot, the last one's (kWrap) to the
