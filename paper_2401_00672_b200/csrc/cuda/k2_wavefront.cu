@@ -864,33 +864,34 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
-      int rot = 0;  // continuous round-robin: slice q of task ti runs on warp (rot_ti + q) mod kNCW
+      int rot = 0;  // round-robin offset (continues across tasks)
       for (int ti = 0; ti < ntask; ti++) {
         const int4 tm = tmeta[ti];
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
         unsigned long long* trp = tr ? a.trace + ((size_t)t * a.ntask_max + ti) * 12 : nullptr;
-        // this warp's first slice of the task; the slices of consecutive tasks continue the
-        // round-robin where the previous task stopped, so task ti's boundary slices land on warps
-        // that are not busy with task ti-1's (their look-ahead overlaps the previous post)
-        const int qw = warp >= rot ? warp - rot : warp - rot + kNCW;
-        rot += ntot % kNCW;
-        rot = rot >= kNCW ? rot - kNCW : rot;
-        if (tr && qw == 0 && lane == 0) trp[0] = gtimer();
-        // LOOK-AHEAD: this warp's first boundary slice of task ti (q = qw).  Its operands and the
+        // this warp's slices of the task: q = qs, qs + qstep, ... < qe
+        int qs, qe, qstep;
+        {
+          // continuous round-robin over all compute warps
+          qs = warp >= rot ? warp - rot : warp - rot + kNCW;
+          qe = ntot;
+          qstep = kNCW;
+          rot += ntot % kNCW;
+          rot = rot >= kNCW ? rot - kNCW : rot;
+        }
+        if (tr && qs == 0 && lane == 0) trp[0] = gtimer();
+        // LOOK-AHEAD: this warp's first boundary slice of task ti (q = qs).  Its operands and the
         // neighbours' values (mailboxes) do not depend on the tile's task ti-1, so they are fetched
         // and awaited BEFORE the barrier that closes task ti-1; only the private x~ reads (post)
         // come after it.  (No deadlock: every slice of task ti-1 this warp owns is done, and the
         // producers of task ti's inputs are rows of earlier steps.)  The slice's chunk must not wait
         // for a ring slot that a slice of task ti frees: chunk g is issued once chunk g - NS is
         // consumed, so it has to lie within NS chunks of the task's first one.
-        const int4 sl0 = smeta[tm.x + (qw < nbnd ? qw : 0)];
-        const bool la = qw < nbnd && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
+        const int4 sl0 = smeta[tm.x + (qs < nbnd && qs < qe ? qs : 0)];
+        const bool la = qs < nbnd && qs < qe && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
         if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
         if (kPrio && !la) named_bar(3, kNC);    // boundary priority
-        // the task's slices (boundary first) round-robin over the compute warps: consecutive
-        // boundary slices land on different SM sub-partitions (their post phases run together
-        // when the neighbours' data arrives); large tasks simply take more rounds
-        for (int q = qw; q < ntot; q += kNCW) {
+        for (int q = qs; q < qe; q += qstep) {
           const bool bnd = q < nbnd;
           const int4 sl = smeta[tm.x + q];
           const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
           const SliceAddr S(blk, R, W, bnd, lane);
           if (kAbl & 16) {
-            if (la && q == qw && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
+            if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
           } else if (bnd) {
 #if POBK_K2_BREG
             BSlice2 B;
@@ -923,14 +924,14 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
 #endif
             if (tr && q == 0 && lane == 0) trp[1] = gtimer();
-            if (la && q == qw && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // look-ahead slice: task ti-1 now complete
+            if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // look-ahead slice: task ti-1 now complete
             if (tr && q == 0 && lane == 0) trp[3] = gtimer();
 #if POBK_K2_BREG
-            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, la && q == qw);
+            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, la && q == qs);
 #else
-            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr, la && q == qw);
+            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr, la && q == qs);
 #endif
-            if (kPrio == 1 && la && q == qw) named_arrive(3, kNC);
+            if (kPrio == 1 && la && q == qs) named_arrive(3, kNC);
             if (tr && q == 0) {
               __syncwarp();
               if (lane == 0) trp[10] = gtimer();
