@@ -120,6 +120,12 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
   const bool k3ok = k3_fits(p, k3b);
   if (k3ok) p.k3_smem = k3b;
   std::string why;
+  if (k3ok && (req == POBK_KERNEL_SMEM || req == POBK_KERNEL_AUTO) && !getenv("POBK_NO_K3E")) {
+    size_t eb = 0;
+    bool built = false;
+    CUDA_TRY(k3e_build(p, rp, col, val, &eb, &built));
+    if (built) p.k3_smem = eb;
+  }
   if (req == POBK_KERNEL_SMEM) {
     if (!k3ok) return fail(POBK_ERR_ARG, "kernel=SMEM requested but the system needs " + std::to_string(k3b) + " B of shared memory");
   } else if (req == POBK_KERNEL_WAVEFRONT) {

@@ -64,6 +64,10 @@ struct Plan {
   size_t k3_smem = 0;
   int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps
   uint8_t* k3_overlap = nullptr;   // [nsteps]
+  int32_t* k3e_col = nullptr;      // K3E thread-major ELL (k3_smem.cu); NULL: K3 reads the CSR
+  double* k3e_val = nullptr;
+  int32_t* k3e_info = nullptr;     // [nsteps*4]
+  int k3e_nent = 0;
 
   std::vector<void*> allocations;
 };
@@ -85,6 +89,8 @@ cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, co
 cudaError_t k1_solve(Plan& p, cudaStream_t s, long long& launches);
 // cuda/k3_smem.cu
 bool k3_fits(const Plan& p, size_t& smem_bytes);
+cudaError_t k3e_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t>& col,
+                      const std::vector<double>& val, size_t* smem_bytes, bool* built);
 cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches);
 // cuda/k2_wavefront.cu
 bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why);

@@ -271,3 +271,28 @@ def test_config5_full_parity(env, b):
     assert np.array_equal(plan.perm(), pre.perm)
     assert np.array_equal(plan.partition()[0], pre.color)
     assert _rel(x, O.run_sweeps(pre, s.f, 20)) <= REL
+
+
+@pytest.mark.parametrize("name,n", [("lap2d5_32", None), ("lap3d7_64", 11), ("randband_20k", 2000), ("geoknn_1m", 3000)])
+def test_k3_layouts_bitwise_equal(env, name, n, monkeypatch):
+    """K3 has two layouts (k3_smem.cu): the thread-major ELL (K3E, rows <= 16 entries) and the CSR
+    fallback (POBK_NO_K3E); both follow the common.cuh contract, so both are the oracle's iterates,
+    bitwise, including RELRES stop decisions at the same sweep."""
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    outs = []
+    for no_e in (False, True):
+        if no_e:
+            monkeypatch.setenv("POBK_NO_K3E", "1")
+        try:
+            _, x, _ = _run(env, s, 17, kernel="smem")
+        except pk.PobkError:
+            pytest.skip("system does not fit one CTA")
+        outs.append(x)
+        plan = pk.Plan.from_system(s, kernel="smem")
+        xr = _dev(torch, np.zeros(s.m))
+        outs.append(plan.solve(_dev(torch, s.f), xr, None, tol=1e-3, stop="relres").sweeps)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    assert np.array_equal(outs[0], O.run_sweeps(pre, s.f, 17))
+    assert np.array_equal(outs[0], outs[2])
+    assert abs(outs[1] - outs[3]) <= 1
