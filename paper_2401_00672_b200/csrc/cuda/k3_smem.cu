@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
   double* nrm2 = (double*)take(8ull * a.m);
   int4* info = (int4*)take(16ull * a.nsteps);
   double* red = (double*)take(64 * 8);
-  __shared__ int s_stop;
 
   const int tid = threadIdx.x;
   for (int i = tid; i < a.nent; i += kENT) { val[i] = a.eval[i]; col[i] = a.ecol[i]; }
@@ -173,13 +172,15 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
   const double tol = a.ctrl->tol, den = a.ctrl->den;
-  if (tid == 0) s_stop = maxs <= 0;
   __syncthreads();
-
+  // stop test value = sqrt(tot)/sqrt(den) < tol; above cut_hi it cannot hold
+  // (margin >> rounding), so the exact value is formed only near the threshold or at the end
+  const double sd = sqrt(den), cut_hi = (den > 0.0 && isfinite(den)) ? (tol * sd) * (tol * sd) * (1.0 + 1e-6) : -1.0;
   long long sweep = 0;
   double value = NAN;
   int term = POBK_TERM_MAX_SWEEPS;
-  while (!s_stop) {
+  bool stop = maxs <= 0;
+  while (!stop) {
     for (int k = 0; k < a.nsteps; k++) {
       const int4 in = info[k];  // {schedule position, rows, W, ELL base}
       for (int r0 = 0; r0 < in.y; r0 += kENT) {
@@ -225,15 +226,25 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
           }
         }
       }
-      const double tot = block_sum<kENT>(loc, red);
-      if (tid == 0) {
-        value = sqrt(tot) / sqrt(den);
-        if (!isfinite(value)) { term = POBK_TERM_NONFINITE; s_stop = 1; }
-        else if (value < tol) { term = POBK_TERM_CONVERGED; s_stop = 1; }
+      // every thread forms the same total (fixed order: warp butterflies, then the 8 warp sums in
+      // order) and takes the stop decision itself: no broadcast barrier.  `red` is next written a
+      // whole sweep (nsteps barriers) later.
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+      if ((tid & 31) == 0) red[tid >> 5] = loc;
+      __syncthreads();
+      double tot = 0.0;
+#pragma unroll
+      for (int w = 0; w < kENT / 32; w++) tot += red[w];
+      // value = sqrt(tot)/sqrt(den) < tol, evaluated exactly only near the threshold
+      // or when the loop ends
+      if (!(tot > cut_hi) || !isfinite(tot) || sweep >= maxs) {
+        value = sqrt(tot) / sd;
+        if (!isfinite(value)) { term = POBK_TERM_NONFINITE; stop = true; }
+        else if (value < tol) { term = POBK_TERM_CONVERGED; stop = true; }
       }
     }
-    if (tid == 0 && !s_stop && sweep >= maxs) { term = POBK_TERM_MAX_SWEEPS; s_stop = 1; }
-    __syncthreads();
+    if (!stop && sweep >= maxs) { term = POBK_TERM_MAX_SWEEPS; stop = true; }
   }
   for (int i = tid; i < a.m; i += kENT) a.xt[i] = x[i];
   if (tid == 0) {
