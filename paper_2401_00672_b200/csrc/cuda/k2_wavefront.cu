@@ -59,13 +59,9 @@
 namespace pobk {
 
 namespace {
-#ifndef POBK_K2_NT
-#define POBK_K2_NT 256
-#endif
-constexpr int kNT = POBK_K2_NT;     // threads per CTA (one CTA per SM)
-constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
-constexpr int kNC = kNCW * 32;      // compute threads
-constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
+// Threads per CTA (one CTA per SM) is a template parameter of k2_sweeps: 256 (7 compute warps,
+// up to 255 registers: register-resident boundary slices, BSlice2) when a task has few slices,
+// 512 (15 compute warps, 128 registers: BSlice) when tasks have many (k2_build decides).
 constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
 static_assert(kSlot <= 65536, "slice offsets are packed in 16 bits");
 constexpr int kMinSlots = 4, kMaxSlots = 12;
@@ -197,14 +193,6 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 __device__ __forceinline__ void named_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-// Boundary priority (POBK_K2_PRIO): after the barrier that closes task k-1, the interior warps
-// wait (named barrier 3) until the look-ahead boundary warps -- the critical path to the
-// neighbouring tiles -- have read their operands (1: after the whole post, 2: after the row sums),
-// so that their shared-memory traffic does not queue behind the interior slices'.
-#ifndef POBK_K2_PRIO
-#define POBK_K2_PRIO 0
-#endif
-constexpr int kPrio = POBK_K2_PRIO;
 // Development ablations (wrong numerics; timing only): bit 0 no mailbox wait, bit 1 no per-task
 // barrier, bit 2 interior slices skipped, bit 3 boundary post skipped, bit 4 every slice skipped,
 // bit 5 no private stores in the boundary write-back, bit 6 weak mailbox stores, bit 7 no re-arm.
@@ -486,7 +474,7 @@ struct BSlice {
   // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
                                        unsigned long long* mbox, unsigned off_p, unsigned off_q, int R,
-                                       unsigned long long* trp, bool arrive) {
+                                       unsigned long long* trp) {
     double s = 0.0, n2 = 0.0;
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
@@ -532,11 +520,6 @@ struct BSlice {
       }
       s = __dadd_rn(s, __dmul_rn(a, x));
       n2 = __dadd_rn(n2, __dmul_rn(a, a));
-    }
-    if (kPrio == 2 && arrive) {
-      double s2 = s;
-      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
-      named_arrive(3, kNC);
     }
     if (trp) {
       double s2 = s;
@@ -617,7 +600,7 @@ __device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, d
       : "r"(p0), "r"(p1), "r"(p2), "r"(p3), "r"(a0), "r"(a1), "r"(a2), "r"(a3));
 }
 
-// Register-resident boundary slice (POBK_K2_BREG, default): the row's columns, values and
+// Register-resident boundary slice (the 256-thread instantiation): the row's columns, values and
 // ||a~||^2 are loaded from the ring BEFORE the barrier that closes the tile's previous task,
 // together with the mailbox poll; after the barrier only the private x~ loads (all in flight at
 // once), the row sum, the division and the write-back remain on the critical path.  Same
@@ -679,8 +662,7 @@ struct BSlice2 {
       if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
-                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
-                                       bool arrive) {
+                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp) {
     // private x~ of entries j < W (final once the tile's previous task is done): all loads in
     // flight before the first use; shared entries keep the polled value; entries >= W are +0
 #pragma unroll
@@ -723,11 +705,6 @@ struct BSlice2 {
       }
       s = __dadd_rn(s, __dmul_rn(a, x));
       n2t = __dadd_rn(n2t, __dmul_rn(a, a));
-    }
-    if (kPrio == 2 && arrive) {
-      double s2 = s;
-      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
-      named_arrive(3, kNC);
     }
     if (trp) {
       double s2 = s;
@@ -782,11 +759,11 @@ struct BSlice2 {
     if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
-#ifndef POBK_K2_BREG
-#define POBK_K2_BREG 1
-#endif
-
+template <int kNT, bool kBReg>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
+  constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
+  constexpr int kNC = kNCW * 32;      // compute threads
+  constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
   extern __shared__ __align__(128) unsigned char smem[];
   const int NS = a.NS;
   unsigned char* ring = smem;                                // NS * kSlot
@@ -890,7 +867,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         const int4 sl0 = smeta[tm.x + (qs < nbnd && qs < qe ? qs : 0)];
         const bool la = qs < nbnd && qs < qe && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
         if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
-        if (kPrio && !la) named_bar(3, kNC);    // boundary priority
         for (int q = qs; q < qe; q += qstep) {
           const bool bnd = q < nbnd;
           const int4 sl = smeta[tm.x + q];
@@ -910,28 +886,27 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           if (kAbl & 16) {
             if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
           } else if (bnd) {
-#if POBK_K2_BREG
-            BSlice2 B;
-            B.pre(S, W);
-            if (tr && q == 0 && lane == 0) trp[8] = gtimer();
             unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
-            B.poll(W, mbox_in);
-#else
-            BSlice B;
-            B.pre(S, W, xb);
-            if (tr && q == 0 && lane == 0) trp[8] = gtimer();
-            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
-            B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
-#endif
-            if (tr && q == 0 && lane == 0) trp[1] = gtimer();
-            if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // look-ahead slice: task ti-1 now complete
-            if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-#if POBK_K2_BREG
-            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, la && q == qs);
-#else
-            if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr, la && q == qs);
-#endif
-            if (kPrio == 1 && la && q == qs) named_arrive(3, kNC);
+            const bool bar = la && q == qs && ti > 0 && !(kAbl & 2);  // look-ahead slice: barrier after the poll
+            if constexpr (kBReg) {
+              BSlice2 B;
+              B.pre(S, W);
+              if (tr && q == 0 && lane == 0) trp[8] = gtimer();
+              B.poll(W, mbox_in);
+              if (tr && q == 0 && lane == 0) trp[1] = gtimer();
+              if (bar) named_bar(1, kNC);
+              if (tr && q == 0 && lane == 0) trp[3] = gtimer();
+              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr);
+            } else {
+              BSlice B;
+              B.pre(S, W, xb);
+              if (tr && q == 0 && lane == 0) trp[8] = gtimer();
+              B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
+              if (tr && q == 0 && lane == 0) trp[1] = gtimer();
+              if (bar) named_bar(1, kNC);
+              if (tr && q == 0 && lane == 0) trp[3] = gtimer();
+              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
+            }
             if (tr && q == 0) {
               __syncwarp();
               if (lane == 0) trp[10] = gtimer();
@@ -1082,6 +1057,7 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 
 struct K2Plan {
   int T = 0, NS = 0;
+  int nt = 256;                // threads per CTA: 256 (BSlice2) or 512 (BSlice), see k2_build
   size_t smem = 0;
   int nsl_max = 1, nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
@@ -1550,6 +1526,11 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   p.k2 = k;
   k->T = T;
   k->NS = NS;
+  // CTA size: each compute warp takes about one slice per task with 7 warps when tasks are small
+  // (register-resident boundary slices, 256 threads); tasks of many slices (config 5: ~16) need
+  // the 15 compute warps of the 512-thread instantiation (measured: 84.6 vs 70.5 us/sweep)
+  k->nt = (double)smeta.size() / std::max<size_t>(tmeta.size(), 1) > 10.0 ? 512 : 256;
+  if (const char* e = getenv("POBK_K2_THREADS")) k->nt = atoi(e) == 512 ? 512 : 256;  // development override
   k->nsl_max = nsl_max;
   k->nck_max = nck_max;
   k->ntask_max = ntask_max;
@@ -1665,9 +1646,9 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const void* fn = (const void*)k2_sweeps;
+  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<256, true>;
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem)) != cudaSuccess) return e;
-  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(kNT), args, k.smem, s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py
     const size_t n = (size_t)k.T * k.ntask_max * 12;
