@@ -1352,8 +1352,10 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
     return false;
   }
   // Bank-aware placement of the private x~ in shared memory.  A warp's access to entry j of its
-  // slice touches one 8-byte word per lane; words w and w' conflict when w = w' (mod 16) (same
-  // bank pair), and the access takes max over residues of the number of distinct words, >= 2.
+  // slice touches one 8-byte word per lane, served per half warp (16 words = one 128-B wavefront);
+  // words w and w' of one half conflict when w = w' (mod 16) (same bank pair), and each half takes
+  // max over residues of the number of distinct words, >= 1 (ncu: 4.5 wavefronts per access with
+  // the former whole-warp model vs an ideal 2).
   // Random placement costs ~5; here each tile's private columns get residues greedily (most
   // accessed first), each residue chosen to minimise the column's collisions with the residues
   // already in its access groups, under a per-residue capacity; local index = residue + 16 * rank.
@@ -1368,15 +1370,19 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       std::vector<int32_t> cols(n);
       std::vector<std::vector<int32_t>> groups_of(n);
       int ng = 0;
+      // an 8-byte warp access is served per HALF warp (lanes 0-15, 16-31: 16 words = 128 B per
+      // wavefront), so an access group is (slice, entry j, half)
       for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
         const auto& rows = slice_rows[si];
         const int W = smeta[si].z;
-        for (int j = 0; j < W; j++, ng++)
-          for (int32_t i : rows)
+        for (int j = 0; j < W; j++, ng += 2)
+          for (size_t r = 0; r < rows.size(); r++) {
+            const int32_t i = rows[r];
             if (j < rlen(i)) {
               const int32_t cg = At.col[At.ptr[i] + j];
-              if (!shared[cg]) groups_of[local[cg]].push_back(ng);
+              if (!shared[cg]) groups_of[local[cg]].push_back(ng + (r >= 16 ? 1 : 0));
             }
+          }
       }
       std::vector<int32_t> gl;  // old local -> global column
       gl.resize(n);
@@ -1412,7 +1418,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
           if (members[g].empty()) continue;
           int a1[16] = {0}, a0[16] = {0}, m1 = 0, m0 = 0;
           for (int x : members[g]) { m1 = std::max(m1, ++a1[res[x]]); m0 = std::max(m0, ++a0[x & 15]); }
-          acc_new += std::max(m1, 2); acc_old += std::max(m0, 2); acc_n += 1;
+          acc_new += std::max(m1, 1); acc_old += std::max(m0, 1); acc_n += 0.5;  // per half warp
         }
       }
       int mx = 0;
