@@ -35,6 +35,16 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 
 // One row of Eq 1.2 by one thread, x in any memory space reachable through a generic pointer.
 // Returns alpha.
+// Products ahead of the chain: in-order issue runs `s = s + a_j*x_j` at ~21 cycles per link when
+// each product is issued next to its add (ptxas keeps the source order), ~8.8 when all products
+// of a row (or batch) are formed first (tools/microbench/mb11.cu).  pin() is a volatile register
+// move that keeps a product where it is written; the additions, and so every rounded result,
+// are unchanged (same operations, same order).
+__device__ __forceinline__ double pin(double v) {
+  asm volatile("mov.b64 %0, %0;" : "+d"(v));
+  return v;
+}
+
 __device__ __forceinline__ double row_project(const int32_t* __restrict__ col, const double* __restrict__ val,
                                               int p0, int p1, double f, double nrm2, double* x) {
   double s = 0.0;

@@ -311,80 +311,8 @@ struct SliceAddr {
 
 // interior slice: every column private (shared memory at xb); pass 2 re-reads x~ from shared
 // memory (unchanged in between: no other row of the category touches these columns)
-#ifndef POBK_K2_ICACHE
-#define POBK_K2_ICACHE 0
-#endif
-constexpr int kICache = POBK_K2_ICACHE;  // interior entries kept in registers between the passes
 __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsigned xb) {
   double s = 0.0, n2 = 0.0;
-  if constexpr (kICache > 0) {
-    // entries j < kICache: column, x~ and value stay in registers for pass 2 (x~ is unchanged in
-    // between: no other row of the category touches these columns)
-    constexpr int kIC = kICache > 0 ? kICache : 1;
-    unsigned cc[kIC];
-    double cx[kIC], ca[kIC];
-#pragma unroll
-    for (int jb = 0; jb < kICache; jb += kBatch) {
-      if (jb < W) {
-        unsigned ad[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
-        unsigned c8[kBatch];
-        lds32x8(c8, ad);
-        double x8[kBatch], a8[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = xb + 8u * c8[u];
-        lds64x8(x8, ad);
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
-        lds64x8(a8, ad);
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {
-          const bool in = jb + u < W;
-          cc[jb + u] = c8[u];
-          ca[jb + u] = in ? a8[u] : 0.0;
-          cx[jb + u] = in ? x8[u] : 0.0;
-          s = __dadd_rn(s, __dmul_rn(ca[jb + u], cx[jb + u]));
-          n2 = __dadd_rn(n2, __dmul_rn(ca[jb + u], ca[jb + u]));
-        }
-      }
-    }
-    for (int jb = kICache; jb < W; jb += kBatch) {
-      unsigned c[kBatch];
-      double av[kBatch], xv[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        const bool in = jb + u < W;
-        const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
-        s = __dadd_rn(s, __dmul_rn(a, x));
-        n2 = __dadd_rn(n2, __dmul_rn(a, a));
-      }
-    }
-    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
-#pragma unroll
-    for (int j = 0; j < kICache; j++)
-      if (j < W) sts64_if(j < S.myl, xb + 8u * cc[j], __dadd_rn(cx[j], __dmul_rn(alpha, ca[j])));
-    for (int jb = kICache; jb < W; jb += kBatch) {
-      unsigned c[kBatch];
-      double av[kBatch], xv[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
-        av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
-    }
-    return;
-  }
   for (int jb = 0; jb < W; jb += kBatch) {
     unsigned c[kBatch];
     double av[kBatch], xv[kBatch];
@@ -395,13 +323,20 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
 #pragma unroll
     for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
     // entries past the slice width contribute +0 * +0 (bit-exact no-ops): no per-entry branches,
-    // so the next batch's loads can issue under this batch's arithmetic
+    // so the next batch's loads can issue under this batch's arithmetic; the batch's products
+    // first, then the two chains (common.cuh pin())
+    double pp[kBatch], qq[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; u++) {
       const bool in = jb + u < W;
       const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
-      s = __dadd_rn(s, __dmul_rn(a, x));
-      n2 = __dadd_rn(n2, __dmul_rn(a, a));
+      pp[u] = pin(__dmul_rn(a, x));
+      qq[u] = pin(__dmul_rn(a, a));
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) {
+      s = __dadd_rn(s, pp[u]);
+      n2 = __dadd_rn(n2, qq[u]);
     }
   }
   const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
@@ -495,13 +430,19 @@ struct BSlice {
         lds64x8(av, ad);
 #pragma unroll
         for (int u = 0; u < kBatch; u++) av[u] = jb + u < W ? av[u] : 0.0;
+        double pp[kBatch], qq[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {  // past the width: +0 * +0 (xr, av are +0 there)
           const int j = jb + u;
           const bool priv = j < W && !(cr[u] & kShared);
           xr[j] = ((shm >> j) & 1u) ? xr[j] : (priv ? xp[u] : 0.0);
-          s = __dadd_rn(s, __dmul_rn(av[u], xr[jb + u]));
-          n2 = __dadd_rn(n2, __dmul_rn(av[u], av[u]));
+          pp[u] = pin(__dmul_rn(av[u], xr[jb + u]));
+          qq[u] = pin(__dmul_rn(av[u], av[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          s = __dadd_rn(s, pp[u]);
+          n2 = __dadd_rn(n2, qq[u]);
         }
       }
     }
@@ -632,8 +573,12 @@ struct BSlice2 {
           av[j] = j < W ? a8[u] : 0.0;
           const bool sh = (c8[u] & kShared) && j < S.myl;
           shm |= sh ? (1u << j) : 0u;
-          n2 = __dadd_rn(n2, __dmul_rn(av[j], av[j]));  // left to right, as the oracle
         }
+        double qq[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) qq[u] = pin(__dmul_rn(av[jb + u], av[jb + u]));
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) n2 = __dadd_rn(n2, qq[u]);  // left to right, as the oracle
       }
     }
   }
@@ -687,8 +632,15 @@ struct BSlice2 {
     }
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < kMaxJ; j++)
-      if ((j & ~(kBatch - 1)) < W) s = __dadd_rn(s, __dmul_rn(av[j], xr[j]));
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // per batch: products first, then the chain
+      if (jb < W) {
+        double pp[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) pp[u] = pin(__dmul_rn(av[jb + u], xr[jb + u]));
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) s = __dadd_rn(s, pp[u]);
+      }
+    }
     double n2t = n2;
     for (int j = kMaxJ; j < W; j++) {  // long rows: entries past the register window
       const unsigned cj = lds32(S.cb + j * S.cs);

@@ -196,10 +196,13 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
 #pragma unroll
           for (int j = 0; j < kEW; j++)
             if (j < W) xv[j] = x[c[j]];
-          double sum = 0.0;
+          double sum = 0.0, pp[kEW];
+#pragma unroll
+          for (int j = 0; j < kEW; j++)  // products first, then the chain (common.cuh pin())
+            if (j < W) pp[j] = pin(__dmul_rn(av[j], xv[j]));
 #pragma unroll
           for (int j = 0; j < kEW; j++)
-            if (j < W) sum = __dadd_rn(sum, __dmul_rn(av[j], xv[j]));
+            if (j < W) sum = __dadd_rn(sum, pp[j]);
           const double alpha = __ddiv_rn(__dsub_rn(f[sidx], sum), nrm2[sidx]);
 #pragma unroll
           for (int j = 0; j < kEW; j++)
