@@ -94,11 +94,8 @@ struct SliceLayout {
 };
 
 struct SyncState {
-  unsigned int arrive[2];
-  int pad0[30];
-  int epoch;  // = sweeps decided
-  int stop;
-  int pad1[30];
+  unsigned int arrive;  // monotonic: T per completed sweep
+  int pad0[31];
 };
 
 struct K2Args {
@@ -136,7 +133,7 @@ struct Ctl {
   int released[kMaxSlots];             // slices consumed per slot (cumulative)
   unsigned long long issued;           // chunks issued (sequence number)
   int stop;
-  int pad;
+  int done;                            // sweeps completed (all tiles stop at the same sweep)
   double part[32];                     // per-compute-warp RSE partials
 };
 
@@ -741,6 +738,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     }
     ctl->issued = 0;
     ctl->stop = 0;
+    ctl->done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < nsl; j += kNT) smeta[j] = a.smeta[s0 + j];
@@ -809,6 +807,15 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           rot = rot >= kNCW ? rot - kNCW : rot;
         }
         if (tr && qs == 0 && lane == 0) trp[0] = gtimer();
+        if (ti == ntask - 1 && warp == kPub && lane == 0 && rse && np > 0) {
+          // the end-of-sweep RSE scan reads this tile's x~* next: bring it into L2 now
+          const char* xs0 = (const char*)(a.xsp + q0);
+          const unsigned bytes = (unsigned)np * 8u;  // multiple of 128 (np: multiple of 16)
+          for (unsigned o = 0; o < bytes; o += 32768u) {
+            const unsigned n = bytes - o < 32768u ? bytes - o : 32768u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs0 + o), "r"(n) : "memory");
+          }
+        }
         // LOOK-AHEAD: this warp's first boundary slice of task ti (q = qs).  Its operands and the
         // neighbours' values (mailboxes) do not depend on the tile's task ti-1, so they are fetched
         // and awaited BEFORE the barrier that closes task ti-1; only the private x~ reads (post)
@@ -880,25 +887,48 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       const bool due = mode == POBK_STOP_RSE && ((sweep % every) == 0 || sweep >= maxs);
       if (due) {
         // columns final for this sweep once the tile's last task is done: the private ones, and
-        // the shared ones whose last writer (row of the highest step) is in this tile
+        // the shared ones whose last writer (row of the highest step) is in this tile.  x~* of the
+        // private columns is contiguous per tile (16-B loads, prefetched into L2 during the
+        // sweep's last task); 4 x 16 B in flight per thread
         double acc = 0.0;
-        const double* xsp = a.xsp + q0;  // x~* of the private columns, in local order (0 at holes)
-        for (int j0 = tid; j0 < np; j0 += 8 * kNC) {  // 8 independent loads in flight per thread
-          double xs[8];
+        const double2* xsp2 = (const double2*)(a.xsp + q0);  // (q0, np: multiples of 16)
+        const int np2 = np >> 1;
+        const double2* xl2 = (const double2*)xloc;
+        for (int j0 = tid; j0 < np2; j0 += 4 * kNC) {
+          double2 xs[4];
 #pragma unroll
-          for (int u = 0; u < 8; u++) xs[u] = j0 + u * kNC < np ? __ldg(xsp + j0 + u * kNC) : 0.0;
+          for (int u = 0; u < 4; u++) xs[u] = j0 + u * kNC < np2 ? __ldg(xsp2 + j0 + u * kNC) : make_double2(0.0, 0.0);
 #pragma unroll
-          for (int u = 0; u < 8; u++)
-            if (j0 + u * kNC < np) {
-              const double d = xloc[j0 + u * kNC] - xs[u];
-              acc = fma(d, d, acc);
+          for (int u = 0; u < 4; u++)
+            if (j0 + u * kNC < np2) {
+              const double2 xv = xl2[j0 + u * kNC];
+              const double d0 = xv.x - xs[u].x, d1 = xv.y - xs[u].y;
+              acc = fma(d0, d0, acc);
+              acc = fma(d1, d1, acc);
             }
         }
+        // owned shared columns: slot indices and x~* first (independent), then the wrap slots --
+        // two dependent global round trips per thread instead of two per element
         const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB;  // sweep = sweeps done
-        for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNC) {
-          const unsigned long long w = ldm_if(1u, wrap + __ldg(a.lastslot + j), 0ull);
-          const double d = __longlong_as_double((long long)w) - __ldg(a.lcx + j);
-          acc = fma(d, d, acc);
+        const int lc1 = a.lastcol_ptr[t + 1];
+        for (int j0 = a.lastcol_ptr[t] + tid; j0 < lc1; j0 += 4 * kNC) {
+          int sl4[4];
+          double xs4[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const bool in = j0 + u * kNC < lc1;
+            sl4[u] = in ? __ldg(a.lastslot + j0 + u * kNC) : 0;
+            xs4[u] = in ? __ldg(a.lcx + j0 + u * kNC) : 0.0;
+          }
+          unsigned long long w4[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) w4[u] = ldm_if(j0 + u * kNC < lc1 ? 1u : 0u, wrap + sl4[u], 0ull);
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            if (j0 + u * kNC < lc1) {
+              const double d = __longlong_as_double((long long)w4[u]) - xs4[u];
+              acc = fma(d, d, acc);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // fixed lane order
@@ -906,50 +936,49 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       }
       named_bar(1, kNC);
       if (warp == kPub) {
+        // grid barrier, one hop: publish the tile's partial, arrive on a monotonic counter, wait
+        // until all T tiles of this sweep have arrived; then EVERY tile forms the same total (fixed
+        // order) and takes the same decision -- no second, releasing hop
         const int par = (int)(sweep & 1);
-        int last = 0;
         if (lane == 0) {
           double part = 0.0;
           if (due)
             for (int w2 = 0; w2 < kNCW; w2++) part += ((volatile double*)ctl->part)[w2];
           a.partials[par * a.T + t] = part;
           __threadfence();
-          last = atomicAdd(&a.sync->arrive[par], 1u) == (unsigned)a.T - 1;
-        }
-        last = __shfl_sync(kFull, last, 0);
-        if (last) {
-          __threadfence();
-          int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
-          double v = 0.0;
-          if (due) {
-            double tot = 0.0;  // fixed order: lane l sums tiles l, l+32, ..., then a fixed butterfly
-            for (int b0 = 0; b0 < a.T; b0 += 32)
-              tot += b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
-            v = sqrt(tot) / sqrt(a.ctrl->den);
-            if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
-            else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
+          atomicAdd(&a.sync->arrive, 1u);
+          const unsigned target = (unsigned)sweep * (unsigned)a.T;
+          while ((unsigned)ld_acquire((const int*)&a.sync->arrive) < target) {
           }
-          if (lane == 0) {
-            a.sync->arrive[par] = 0;
-            a.sync->stop = st;
+        }
+        __syncwarp();
+        (void)ld_acquire((const int*)&a.sync->arrive);  // (each lane: acquire before reading partials)
+        int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
+        double v = 0.0;
+        if (due) {
+          double tot = 0.0;  // fixed order: lane l sums tiles l, l+32, ..., then a fixed butterfly
+          for (int b0 = 0; b0 < a.T; b0 += 32)
+            tot += b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+          v = sqrt(tot) / sqrt(a.ctrl->den);
+          if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
+          else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
+        }
+        if (lane == 0) {
+          if (st && t == 0) {  // (every tile holds the same values)
             if (due) a.ctrl->value = v;
             a.ctrl->sweeps = sweep;
             a.ctrl->term = term;
-            st_release(&a.sync->epoch, (int)sweep);
           }
-        } else if (lane == 0) {
-          while (ld_acquire(&a.sync->epoch) < (int)sweep) {
-          }
+          *(volatile int*)&ctl->stop = st;
         }
-        int stop = 0;
-        if (lane == 0) stop = ld_relaxed(&a.sync->stop);
-        stop = __shfl_sync(kFull, stop, 0);
-        if (lane == 0) *(volatile int*)&ctl->stop = stop;
       }
       named_bar(2, kNC);
-      if (ld_vol_shared(&ctl->stop)) break;
+      if (ld_vol_shared(&ctl->stop)) {
+        if (tid == 0) ctl->done = (int)sweep;
+        break;
+      }
     }
   }
   __syncthreads();
@@ -958,7 +987,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     if (gcol >= 0) a.xg[gcol] = xloc[j];
   }
   {  // shared columns owned by this tile: their final value sits in the last sweep's wrap slot
-    const long long done = ld_relaxed(&a.sync->epoch);
+    const long long done = min(maxs, (long long)ctl->done);
     const unsigned long long* wrap = a.mbox + (size_t)(done & 1) * a.NB;
     for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNT)
       a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + a.lastslot[j], 0ull));
@@ -979,11 +1008,7 @@ __global__ void k2_gather_xs(int n, const int* __restrict__ pmap, int nl, const 
   }
 }
 
-__global__ void k2_reset(SyncState* sync) {
-  sync->arrive[0] = sync->arrive[1] = 0;
-  sync->epoch = 0;
-  sync->stop = 0;
-}
+__global__ void k2_reset(SyncState* sync) { sync->arrive = 0; }
 
 // every mailbox slot empty, then each shared column's first reader of sweep 0 gets x~0
 __global__ void k2_mbox_fill(unsigned long long* mbox, long long n) {
