@@ -202,6 +202,9 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 #ifndef POBK_K2_POLLSLEEP
 #define POBK_K2_POLLSLEEP 0  // back-off between mailbox poll rounds (ns)
 #endif
+#ifndef POBK_K2_PRIO
+#define POBK_K2_PRIO 1  // boundary priority on the 256-thread path (measured 1-2% faster, configs 3-4)
+#endif
 #ifndef POBK_K2_ABL
 #define POBK_K2_ABL 0
 #endif
@@ -604,7 +607,8 @@ struct BSlice2 {
       if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
-                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp) {
+                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
+                                       int prio = 0) {
     // private x~ of entries j < W (final once the tile's previous task is done): all loads in
     // flight before the first use; shared entries keep the polled value; entries >= W are +0
 #pragma unroll
@@ -622,6 +626,13 @@ struct BSlice2 {
         lds64x4_if(xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3], p[0], p[1], p[2], p[3], ad[0], ad[1], ad[2], ad[3]);
       }
     }
+#if POBK_K2_PRIO
+    if (prio) {  // operands in registers: let the interior warps at the shared-memory pipe
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[j]));
+      named_arrive(3, prio);
+    }
+#endif
     if (POBK_K2_FT && trp) {  // all private x~ loads complete
 #pragma unroll
       for (int j = 0; j < kMaxJ; j++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[j]));
@@ -826,6 +837,11 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         const int4 sl0 = smeta[tm.x + (qs < nbnd && qs < qe ? qs : 0)];
         const bool la = qs < nbnd && qs < qe && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
         if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
+#if POBK_K2_PRIO
+        // boundary priority: the interior warps start the task once the look-ahead warps hold
+        // their private operands (barrier 3: look-ahead warps arrive, the others sync)
+        if (kBReg && !la) named_bar(3, kNC);
+#endif
         for (int q = qs; q < qe; q += qstep) {
           const bool bnd = q < nbnd;
           const int4 sl = smeta[tm.x + q];
@@ -855,7 +871,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (tr && q == 0 && lane == 0) trp[1] = gtimer();
               if (bar) named_bar(1, kNC);
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr);
+              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs) ? kNC : 0);
             } else {
               BSlice B;
               B.pre(S, W, xb);
