@@ -172,6 +172,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 #ifndef POBK_K2_FT
 #define POBK_K2_FT 0
 #endif
+// POBK_K2_WT (development): per task, every compute warp's clock64 at its arrival at the barrier
+// that closes the task (slots 0..6 of the task's record), slot 7: look-ahead warps of the next
+// task (bit mask), slot 8: the barrier's release (tools/k2_wt.py; 256-thread instantiation; the
+// other trace stamps share the record, so only slots 0..8 are meaningful in this mode)
+#ifndef POBK_K2_WT
+#define POBK_K2_WT 0
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long v;
   if (POBK_K2_FT)
@@ -836,7 +843,13 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         // consumed, so it has to lie within NS chunks of the task's first one.
         const int4 sl0 = smeta[tm.x + (qs < nbnd && qs < qe ? qs : 0)];
         const bool la = qs < nbnd && qs < qe && (sl0.x & 0xfffff) - (smeta[tm.x].x & 0xfffff) < NS;
+        unsigned long long* const wtp = (POBK_K2_WT && tr && ti > 0) ? a.trace + ((size_t)t * a.ntask_max + ti - 1) * 12 : nullptr;
+        if (POBK_K2_WT && wtp && lane == 0 && warp < 8) {
+          wtp[warp] = clock64();
+          if (la) atomicOr(&wtp[7], 1ull << warp);
+        }
         if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
+        if (POBK_K2_WT && wtp && lane == 0 && warp == 0 && !la) wtp[8] = clock64();
 #if POBK_K2_PRIO
         // boundary priority: the interior warps start the task once the look-ahead warps hold
         // their private operands (barrier 3: look-ahead warps arrive, the others sync)
@@ -869,7 +882,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (tr && q == 0 && lane == 0) trp[8] = gtimer();
               B.poll(W, mbox_in);
               if (tr && q == 0 && lane == 0) trp[1] = gtimer();
+              if (POBK_K2_WT && bar && wtp && lane == 0 && warp < 8) wtp[warp] = clock64();
               if (bar) named_bar(1, kNC);
+              if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
               if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs) ? kNC : 0);
             } else {
@@ -878,7 +893,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (tr && q == 0 && lane == 0) trp[8] = gtimer();
               B.poll(S, W, R, mbox_in, (tr && q == 0) ? trp : nullptr);
               if (tr && q == 0 && lane == 0) trp[1] = gtimer();
+              if (POBK_K2_WT && bar && wtp && lane == 0 && warp < 8) wtp[warp] = clock64();
               if (bar) named_bar(1, kNC);
+              if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
               if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
             }
