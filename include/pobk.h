@@ -71,7 +71,8 @@ enum {
   POBK_KERNEL_AUTO = 0,
   POBK_KERNEL_LAUNCH = 1,    /* K1: one launch per category step, device-driven CUDA-graph loop */
   POBK_KERNEL_WAVEFRONT = 2, /* K2: persistent tiled wavefront, x~ tile-private in shared memory */
-  POBK_KERNEL_SMEM = 3       /* K3: one CTA, whole system resident in shared memory */
+  POBK_KERNEL_SMEM = 3,      /* K3: one CTA, whole system resident in shared memory */
+  POBK_KERNEL_CLUSTER = 4    /* K4: one thread-block cluster, system in distributed shared memory */
 };
 
 typedef struct {

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libpobk.so")
 OK, ERR_ARG, ERR_BAD_CSR, ERR_ZERO_ROW, ERR_UNSTABLE_THR, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(8)
 TERM_CONVERGED, TERM_MAX_SWEEPS, TERM_NONFINITE = 0, 1, 2
 STOP = {"rse": 0, "relres": 1, "none": 2}
-KERNEL = {"auto": 0, "launch": 1, "wavefront": 2, "smem": 3}
+KERNEL = {"auto": 0, "launch": 1, "wavefront": 2, "smem": 3, "cluster": 4}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 TERM_NAME = {TERM_CONVERGED: "converged", TERM_MAX_SWEEPS: "max_sweeps", TERM_NONFINITE: "nonfinite"}
 

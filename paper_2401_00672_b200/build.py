@@ -25,6 +25,7 @@ SOURCES = [
     "cuda/k1_launch.cu",
     "cuda/k3_smem.cu",
     "cuda/k2_wavefront.cu",
+    "cuda/k4_cluster.cu",
 ]
 HEADERS = ["internal.h", "plan.h", "cuda/common.cuh", "../../include/pobk.h"]
 

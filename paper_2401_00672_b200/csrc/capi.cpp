@@ -63,6 +63,7 @@ void destroy_plan(Plan* p) {
   if (p->device >= 0) {
     DeviceGuard g(p->device);
     if (p->k2) k2_free(*p);
+    if (p->k4) k4_free(*p);
     if (p->k1_exec) cudaGraphExecDestroy(p->k1_exec);
     if (p->k1_graph) cudaGraphDestroy(p->k1_graph);
     for (void* a : p->allocations) cudaFree(a);
@@ -131,7 +132,11 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
   } else if (req == POBK_KERNEL_WAVEFRONT) {
     if (p.any_overlap) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT does not support overlapping categories (thr > 0)");
     if (!k2_build(p, At, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
+  } else if (req == POBK_KERNEL_CLUSTER) {
+    if (!k4_build(p, rp, col, val, why)) return fail(POBK_ERR_ARG, "kernel=CLUSTER unavailable: " + why);
   } else if (req == POBK_KERNEL_AUTO) {
+    // K3 (one CTA) when the system fits one CTA's shared memory, else the K2 wavefront from
+    // m >= 4096, else K1 (K4, one cluster, is explicit-only: slower than K2 where both apply)
     if (k3ok) p.kernel = POBK_KERNEL_SMEM;
     else if (!p.any_overlap && m >= 4096 && k2_build(p, At, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
     else p.kernel = POBK_KERNEL_LAUNCH;
@@ -154,6 +159,7 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
     switch (used) {
       case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
       case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, f, s, launches)); break;
+      case POBK_KERNEL_CLUSTER: CUDA_TRY(k4_solve(p, s, launches)); break;
       default: CUDA_TRY(k1_solve(p, s, launches)); break;
     }
   }
@@ -231,7 +237,7 @@ pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* co
   pobk_preprocess_opts_default(&o);
   if (opts) o = *opts;
   if (!(o.thr >= 0.0 && o.thr < 1.0)) return fail(POBK_ERR_ARG, "opts.thr must be in [0, 1)");
-  if (o.kernel < POBK_KERNEL_AUTO || o.kernel > POBK_KERNEL_SMEM) return fail(POBK_ERR_ARG, "opts.kernel out of range");
+  if (o.kernel < POBK_KERNEL_AUTO || o.kernel > POBK_KERNEL_CLUSTER) return fail(POBK_ERR_ARG, "opts.kernel out of range");
   if (device < -1) return fail(POBK_ERR_ARG, "device must be >= -1");
   try {
     auto t0 = std::chrono::steady_clock::now();

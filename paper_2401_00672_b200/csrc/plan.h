@@ -21,6 +21,7 @@ struct DevCSR {
 };
 
 struct K2Plan;  // cuda/k2_wavefront.cu
+struct K4Plan;  // cuda/k4_cluster.cu
 
 struct Plan {
   int device = -1;
@@ -61,6 +62,7 @@ struct Plan {
   long long k1_nodes_per_sweep = 0;
 
   K2Plan* k2 = nullptr;
+  K4Plan* k4 = nullptr;
   size_t k3_smem = 0;
   int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps
   uint8_t* k3_overlap = nullptr;   // [nsteps]
@@ -92,6 +94,12 @@ bool k3_fits(const Plan& p, size_t& smem_bytes);
 cudaError_t k3e_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t>& col,
                       const std::vector<double>& val, size_t* smem_bytes, bool* built);
 cudaError_t k3_solve(Plan& p, cudaStream_t s, long long& launches);
+// cuda/k4_cluster.cu
+bool k4_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t>& col, const std::vector<double>& val,
+              std::string& why);
+cudaError_t k4_solve(Plan& p, cudaStream_t s, long long& launches);
+void k4_free(Plan& p);
+int k4_cluster_size(const Plan& p);
 // cuda/k2_wavefront.cu
 bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why);
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);

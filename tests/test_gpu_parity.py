@@ -45,7 +45,7 @@ SMALL = [("lap2d5_32", None), ("randband_20k", None), ("lap3d7_64", 20), ("geokn
          ("batch9pt_1024", 100)]
 
 
-@pytest.mark.parametrize("kernel", ["launch", "smem", "wavefront", "auto"])
+@pytest.mark.parametrize("kernel", ["launch", "smem", "cluster", "wavefront", "auto"])
 @pytest.mark.parametrize("name,n", SMALL)
 def test_fixed_sweeps_parity(env, name, n, kernel):
     s = gen.make(name, n=n) if n else gen.make(name)
@@ -54,7 +54,7 @@ def test_fixed_sweeps_parity(env, name, n, kernel):
     try:
         plan = pk.Plan.from_system(s, kernel=kernel)
     except pk.PobkError as e:
-        if kernel in ("smem", "wavefront") and e.code == 1:
+        if kernel in ("smem", "cluster", "wavefront") and e.code == 1:
             pytest.skip(f"{kernel} not applicable: {e}")
         raise
     assert np.array_equal(plan.perm(), pre.perm)
@@ -73,7 +73,7 @@ def test_kernel_families_bitwise_equal(env, name, n):
     pk, _ = env
     s = gen.make(name, n=n) if n else gen.make(name)
     outs = {}
-    for kernel in ("launch", "smem", "wavefront"):
+    for kernel in ("launch", "smem", "cluster", "wavefront"):
         try:
             _, outs[kernel], _ = _run(env, s, 12, kernel=kernel)
         except pk.PobkError:
