@@ -163,7 +163,8 @@ class Plan:
 
 def solve_batch(plans, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse",
                 check_every: int = 1, stream=None) -> list[Report]:
-    """pobk_solve_batch: independent systems on one device, back to back on one stream."""
+    """pobk_solve_batch: independent systems on one device (two concurrent lanes when every plan is a
+    K2 plan filling at most half the SMs, e.g. built with tile_rows = half_gpu_tile_rows(m))."""
     nb = len(plans)
     H = (ctypes.c_void_p * nb)(*[p._h.value for p in plans])
     F = (ctypes.c_void_p * nb)(*[_dev_ptr(f, "f", p.m).value for f, p in zip(fs, plans)])
@@ -175,3 +176,11 @@ def solve_batch(plans, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int 
                                    ctypes.cast(XS, ctypes.c_void_p) if XS is not None else None, ctypes.byref(o),
                                    _stream(stream), ctypes.cast(reps, ctypes.c_void_p)))
     return list(reps)
+
+
+def half_gpu_tile_rows(m: int, device: int | None = None) -> int:
+    """tile_rows for a K2 plan whose tiles fill at most half of the device's SMs (batched solves
+    then run two systems concurrently, pobk_solve_batch)."""
+    import torch
+    sms = torch.cuda.get_device_properties(device if device is not None else torch.cuda.current_device()).multi_processor_count
+    return -(-int(m) // max(1, sms // 2 - 2))

@@ -144,8 +144,10 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
   return POBK_OK;
 }
 
+pobk_status solve_finish(Plan& p, const pobk_solve_opts& o, pobk_report* rep);
+
 pobk_status solve_device(Plan& p, const double* f, double* x, const double* xstar, const pobk_solve_opts& o,
-                         cudaStream_t s, pobk_report* rep) {
+                         cudaStream_t s, pobk_report* rep, bool defer = false) {
   long long launches = 0;
   CUDA_TRY(cudaEventRecord(p.ev[0], s));
   CUDA_TRY(launch_permute_in(p, f, x, xstar, p.d_fs, p.d_xt, o.stop == POBK_STOP_RSE ? p.d_xst : nullptr, s, launches));
@@ -167,7 +169,17 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
   CUDA_TRY(launch_permute_out(p, x, s, launches));
   CUDA_TRY(cudaEventRecord(p.ev[3], s));
   CUDA_TRY(cudaMemcpyAsync(p.h_ctrl, p.d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+  p.pending_launches = launches;
+  p.pending_used = used;
+  if (defer) return POBK_OK;  // (batch: the caller synchronises, then solve_finish)
   CUDA_TRY(cudaStreamSynchronize(s));
+  return solve_finish(p, o, rep);
+}
+
+// the report of a solve enqueued by solve_device (its stream synchronised)
+pobk_status solve_finish(Plan& p, const pobk_solve_opts& o, pobk_report* rep) {
+  long long launches = p.pending_launches;
+  const int used = p.pending_used;
   float t_all = 0.f, t_sw = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&t_all, p.ev[0], p.ev[3]));
   CUDA_TRY(cudaEventElapsedTime(&t_sw, p.ev[1], p.ev[2]));
@@ -386,12 +398,68 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
                              const double* const* xstar, const pobk_solve_opts* opts, void* stream, pobk_report* reps) {
   g_err.clear();
   if (nb < 0 || (nb > 0 && (!plans || !f || !x))) return fail(POBK_ERR_ARG, "bad batch arguments");
+  // Lanes: when every system is a K2 plan on the same device and nl >= 2 of their grids fit side
+  // by side (e.g. plans built with half-GPU tiles), system b runs on internal stream b mod nl, so
+  // nl cooperative sweep kernels share the GPU (each system's latency-bound step chain overlaps
+  // the others').  Results are those of back-to-back solves (tiling never changes them).
+  bool lanes = nb >= 2;
+  int sms = 148, dev = -1;
+  for (int32_t b = 0; b < nb && lanes; b++) {
+    if (!plans[b] || plans[b]->device < 0 || plans[b]->kernel != POBK_KERNEL_WAVEFRONT || !plans[b]->k2) lanes = false;
+    else if (dev >= 0 && plans[b]->device != dev) lanes = false;
+    else dev = plans[b]->device;
+  }
+  int nl = 1;  // lanes: as many K2 grids as fit side by side (at most 4)
+  if (lanes) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) sms = prop.multiProcessorCount;
+    int tmax = 1;
+    for (int32_t b = 0; b < nb; b++) tmax = std::max(tmax, (int)plans[b]->ntiles);
+    nl = std::min({4, sms / tmax, (int)nb});
+    lanes = nl >= 2 && !getenv("POBK_BATCH_SERIAL");
+  }
+  if (!lanes) {
+    for (int32_t b = 0; b < nb; b++) {
+      pobk_status st = pobk_solve(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
+      if (st != POBK_OK) {
+        g_err = "system " + std::to_string(b) + ": " + g_err;
+        return st;
+      }
+    }
+    return POBK_OK;
+  }
+  DeviceGuard g(dev);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  static thread_local int lane_dev = -1;
+  static thread_local cudaStream_t lane_s[4] = {nullptr, nullptr, nullptr, nullptr};
+  static thread_local cudaEvent_t lane_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (lane_dev != dev) {  // (per thread and device; created once)
+    for (int i = 0; i < 4; i++) CUDA_TRY(cudaStreamCreateWithFlags(&lane_s[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 5; i++) CUDA_TRY(cudaEventCreateWithFlags(&lane_ev[i], cudaEventDisableTiming));
+    lane_dev = dev;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaEventRecord(lane_ev[4], s));
+  for (int i = 0; i < nl; i++) CUDA_TRY(cudaStreamWaitEvent(lane_s[i], lane_ev[4], 0));
+  std::vector<pobk_solve_opts> os(nb);
   for (int32_t b = 0; b < nb; b++) {
-    pobk_status st = pobk_solve(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
+    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
+    if (st == POBK_OK)
+      st = solve_device(*plans[b], f[b], x[b], os[b].stop == POBK_STOP_RSE && xstar ? xstar[b] : nullptr, os[b], lane_s[b % nl],
+                        nullptr, true);
     if (st != POBK_OK) {
       g_err = "system " + std::to_string(b) + ": " + g_err;
       return st;
     }
+  }
+  for (int i = 0; i < nl; i++) {
+    CUDA_TRY(cudaEventRecord(lane_ev[i], lane_s[i]));
+    CUDA_TRY(cudaStreamWaitEvent(s, lane_ev[i], 0));
+  }
+  for (int i = 0; i < nl; i++) CUDA_TRY(cudaStreamSynchronize(lane_s[i]));
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = solve_finish(*plans[b], os[b], reps ? reps + b : nullptr);
+    if (st != POBK_OK) return st;
   }
   return POBK_OK;
 }

@@ -1246,7 +1246,10 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   // private columns per tile (ascending), capped so that kMinSlots ring slots still fit
   const size_t fixed = sizeof(Ctl) + 128;
   // (16 B per column: conservative -- x~ takes 8 -- so that tiles keep a deep TMA ring)
-  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / 16 / 1.04) - 48;
+  // bytes of shared memory budgeted per private column: 8 (x~ only; the ring takes what remains,
+  // at least kMinSlots slots), so that half-GPU tilings (batched solves on two lanes) stay private
+  const int pcb = getenv("POBK_K2_PCB") ? std::max(8, atoi(getenv("POBK_K2_PCB"))) : 8;
+  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / pcb / 1.04) - 48;
   std::vector<int32_t> local(m, -1);
   std::vector<int> pmap_ptr(T + 1, 0);
   std::vector<int> pmap;

@@ -62,6 +62,8 @@ struct Plan {
   long long k1_nodes_per_sweep = 0;
 
   K2Plan* k2 = nullptr;
+  long long pending_launches = 0;  // solve_device -> solve_finish (batched solves)
+  int pending_used = 0;
   K4Plan* k4 = nullptr;
   size_t k3_smem = 0;
   int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps

@@ -18,7 +18,8 @@ peak = json.load(open("MEASURED_PEAKS.json")).get("hbm_gbs", 6650.0) if os.path.
 rows = []
 for name in ["lap2d5_32", "randband_20k", "lap3d7_64", "geoknn_1m", "batch9pt_1024"]:
     systems = [gen.make(name, b) for b in range(8)] if name == "batch9pt_1024" else [gen.make(name)]
-    plans = [pk.Plan.from_system(s) for s in systems]
+    tr = pk.half_gpu_tile_rows(systems[0].m) if len(systems) > 1 else 0  # batched: two concurrent lanes
+    plans = [pk.Plan.from_system(s, tile_rows=tr) for s in systems]
     fs = [torch.from_numpy(s.f).cuda() for s in systems]
     xst = [torch.from_numpy(s.x_star).cuda() for s in systems]
     xs = [torch.zeros(s.m, dtype=torch.float64, device="cuda") for s in systems]
