@@ -1666,7 +1666,14 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   }
   void* args[] = {&a};
   const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<256, true>;
-  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem)) != cudaSuccess) return e;
+  // the attribute is raised once to the whole budget (never changed between launches: changing a
+  // function's attribute while another lane's grid of it runs can serialise the lanes)
+  static int attr_set[2] = {0, 0};
+  int& done = attr_set[k.nt == 512 ? 1 : 0];
+  if (!done) {
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal)) != cudaSuccess) return e;
+    done = 1;
+  }
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py

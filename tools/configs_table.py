@@ -16,7 +16,8 @@ from bench import TOL, cpu_model
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/configs.md"
 peak = json.load(open("MEASURED_PEAKS.json")).get("hbm_gbs", 6650.0) if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 rows = []
-for name in ["lap2d5_32", "randband_20k", "lap3d7_64", "geoknn_1m", "batch9pt_1024"]:
+names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["lap2d5_32", "randband_20k", "lap3d7_64", "geoknn_1m", "batch9pt_1024"]
+for name in names:
     systems = [gen.make(name, b) for b in range(8)] if name == "batch9pt_1024" else [gen.make(name)]
     tr = pk.half_gpu_tile_rows(systems[0].m) if len(systems) > 1 else 0  # batched: two concurrent lanes
     plans = [pk.Plan.from_system(s, tile_rows=tr) for s in systems]
