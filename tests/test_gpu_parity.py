@@ -237,6 +237,29 @@ def test_batch_equals_single(env):
         assert r1.sweeps == r.sweeps and np.array_equal(x.cpu().numpy(), xb.cpu().numpy())
 
 
+@pytest.mark.parametrize("nb", [2, 5])
+def test_batch_lanes_equal_single(env, nb):
+    """Concurrent lanes (pobk_solve_batch with half-GPU K2 tilings): every system's stop sweep,
+    final RSE and iterates are bitwise those of its own back-to-back solve, and of the oracle's
+    sweeps (config-5 generator at m = 160^2, odd and even batch sizes)."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b, n=160) for b in range(nb)]
+    tr = pk.half_gpu_tile_rows(systems[0].m)
+    plans = [pk.Plan.from_system(s, kernel="wavefront", tile_rows=tr) for s in systems]
+    assert all(2 * p.layout_stats()["ntiles"] <= torch.cuda.get_device_properties(0).multi_processor_count for p in plans)
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = pk.solve_batch(plans, [_dev(torch, s.f) for s in systems], xs, [_dev(torch, s.x_star) for s in systems],
+                          tol=0.2)
+    for s, p, xb, r in zip(systems, plans, xs, reps):
+        x = _dev(torch, np.zeros(s.m))
+        r1 = p.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=0.2)
+        assert r1.sweeps == r.sweeps and r1.final_value == r.final_value
+        assert np.array_equal(x.cpu().numpy(), xb.cpu().numpy())
+    s0 = systems[0]
+    pre = O.preprocess(s0.m, s0.indptr, s0.indices, s0.data)
+    assert np.array_equal(xs[0].cpu().numpy(), O.run_sweeps(pre, s0.f, reps[0].sweeps))
+
+
 # ---------------------------------------------------------------- full BASELINE sizes
 @pytest.mark.slow
 def test_config3_full_parity(env):
