@@ -155,8 +155,12 @@ pobk_status pobk_solve(pobk_plan_t plan, const double* f_dev, double* x_dev, con
 pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const double* xstar,
                             const pobk_solve_opts* opts, void* stream, pobk_report* rep);
 
-/* nb independent systems (one plan each, same device), solved back to back on `stream`; every
- * system stops on its own rule.  Arrays of nb device pointers; reps[nb]. */
+/* nb independent systems (one plan each, same device); every system stops on its own rule.
+ * Arrays of nb device pointers; reps[nb].  Ordered after prior work on `stream`, and `stream`
+ * waits for all of them.  When every plan is a K2 (wavefront) plan and L >= 2 of their grids fit
+ * the device side by side (plans built with tile_rows covering at most 1/L of the SMs), system b
+ * runs on internal stream b mod L (concurrent cooperative sweep kernels); otherwise back to back
+ * on `stream`.  Results are identical either way.  Blocks until reps are filled. */
 pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const* f_dev, double* const* x_dev,
                              const double* const* xstar_dev, const pobk_solve_opts* opts, void* stream,
                              pobk_report* reps);
