@@ -411,8 +411,8 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
   }
   int nl = 1;  // lanes: as many K2 grids as fit side by side (at most 4)
   if (lanes) {
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) sms = prop.multiProcessorCount;
+    int v = 0;  // (cudaGetDeviceProperties costs milliseconds; the attribute query does not)
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
     int tmax = 1;
     for (int32_t b = 0; b < nb; b++) tmax = std::max(tmax, (int)plans[b]->ntiles);
     nl = std::min({4, sms / tmax, (int)nb});
