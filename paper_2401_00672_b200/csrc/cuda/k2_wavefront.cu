@@ -212,6 +212,9 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 #ifndef POBK_K2_PRIO
 #define POBK_K2_PRIO 1  // boundary priority on the 256-thread path (measured 1-2% faster, configs 3-4)
 #endif
+#ifndef POBK_K2_NTB
+#define POBK_K2_NTB 256  // threads of the register-resident (BSlice2) instantiation
+#endif
 #ifndef POBK_K2_ABL
 #define POBK_K2_ABL 0
 #endif
@@ -1667,7 +1670,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<256, true>;
+  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<POBK_K2_NTB, true>;
   // the attribute is raised once to the whole budget (never changed between launches: changing a
   // function's attribute while another lane's grid of it runs can serialise the lanes)
   static int attr_set[2] = {0, 0};
@@ -1676,7 +1679,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal)) != cudaSuccess) return e;
     done = 1;
   }
-  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
+  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt == 512 ? 512 : POBK_K2_NTB), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py
     const size_t n = (size_t)k.T * k.ntask_max * 12;
