@@ -146,6 +146,34 @@ size_t k3e_bytes(int m, int nent, int nsteps) {
          align16(16ull * nsteps) + 64 * 8;
 }
 
+// One row of K3E: entries j < EW at e0 + j*kENT; entries j >= W are padding (the zero slot m,
+// value +0) selected without branches, so all operand loads of the row issue back to back.
+template <int EW>
+__device__ __forceinline__ void k3e_row(const int32_t* col, const double* val, double* x, int e0, int W, double fi,
+                                        double ni, int m) {
+  int c[EW];
+  double av[EW], xv[EW];
+#pragma unroll
+  for (int j = 0; j < EW; j++) {
+    const int jj = j < W ? j : W - 1;
+    const int cj = col[e0 + jj * kENT];
+    const double aj = val[e0 + jj * kENT];
+    c[j] = j < W ? cj : m;
+    av[j] = j < W ? aj : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < EW; j++) xv[j] = x[c[j]];
+  double sum = 0.0, pp[EW];
+#pragma unroll
+  for (int j = 0; j < EW; j++) pp[j] = pin(__dmul_rn(av[j], xv[j]));  // products first (common.cuh)
+#pragma unroll
+  for (int j = 0; j < EW; j++) sum = __dadd_rn(sum, pp[j]);  // (+0 * +0 past W: no-ops)
+  const double alpha = __ddiv_rn(__dsub_rn(fi, sum), ni);
+#pragma unroll
+  for (int j = 0; j < EW; j++)
+    if (c[j] < m) x[c[j]] = __dadd_rn(xv[j], __dmul_rn(alpha, av[j]));
+}
+
 __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* q = smem;
@@ -188,25 +216,8 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
         if (rr < in.y) {
           const int sidx = in.x + rr, W = in.z;
           const int e0 = in.w + (r0 / kENT) * W * kENT + tid;
-          int c[kEW];
-          double av[kEW], xv[kEW];
-#pragma unroll
-          for (int j = 0; j < kEW; j++)
-            if (j < W) { c[j] = col[e0 + j * kENT]; av[j] = val[e0 + j * kENT]; }
-#pragma unroll
-          for (int j = 0; j < kEW; j++)
-            if (j < W) xv[j] = x[c[j]];
-          double sum = 0.0, pp[kEW];
-#pragma unroll
-          for (int j = 0; j < kEW; j++)  // products first, then the chain (common.cuh pin())
-            if (j < W) pp[j] = pin(__dmul_rn(av[j], xv[j]));
-#pragma unroll
-          for (int j = 0; j < kEW; j++)
-            if (j < W) sum = __dadd_rn(sum, pp[j]);
-          const double alpha = __ddiv_rn(__dsub_rn(f[sidx], sum), nrm2[sidx]);
-#pragma unroll
-          for (int j = 0; j < kEW; j++)
-            if (j < W && c[j] < a.m) x[c[j]] = __dadd_rn(xv[j], __dmul_rn(alpha, av[j]));
+          if (W <= 8) k3e_row<8>(col, val, x, e0, W, f[sidx], nrm2[sidx], a.m);
+          else k3e_row<kEW>(col, val, x, e0, W, f[sidx], nrm2[sidx], a.m);
         }
       }
       __syncthreads();
