@@ -215,6 +215,9 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 #ifndef POBK_K2_NTB
 #define POBK_K2_NTB 256  // threads of the register-resident (BSlice2) instantiation
 #endif
+#ifndef POBK_K2_BREGB
+#define POBK_K2_BREGB 1  // development: 0 = that instantiation uses BSlice
+#endif
 #ifndef POBK_K2_ABL
 #define POBK_K2_ABL 0
 #endif
@@ -1670,7 +1673,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<POBK_K2_NTB, true>;
+  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<POBK_K2_NTB, POBK_K2_BREGB != 0>;
   // the attribute is raised once to the whole budget (never changed between launches: changing a
   // function's attribute while another lane's grid of it runs can serialise the lanes)
   static int attr_set[2] = {0, 0};
