@@ -296,6 +296,25 @@ def test_config5_full_parity(env, b):
     assert _rel(x, O.run_sweeps(pre, s.f, 20)) <= REL
 
 
+@pytest.mark.slow
+def test_config5_full_parity_bench_launch(env):
+    """Config 5 at full size in the bench's launch configuration: systems 0 and 63 in one
+    pobk_solve_batch call on two lanes (half-GPU K2 tilings), N_fix = 20 sweeps; bit-exact
+    permutation / partition and iterates bitwise equal to the oracle's."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b) for b in (0, 63)]
+    tr = pk.half_gpu_tile_rows(systems[0].m)
+    plans = [pk.Plan.from_system(s, tile_rows=tr) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = pk.solve_batch(plans, [_dev(torch, s.f) for s in systems], xs, [_dev(torch, s.x_star) for s in systems],
+                          max_sweeps=20, stop="none")
+    for s, p, x, r in zip(systems, plans, xs, reps):
+        assert r.sweeps == 20
+        pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+        assert np.array_equal(p.perm(), pre.perm) and np.array_equal(p.partition()[0], pre.color)
+        assert np.array_equal(x.cpu().numpy(), O.run_sweeps(pre, s.f, 20))
+
+
 @pytest.mark.parametrize("name,n", [("lap2d5_32", None), ("lap3d7_64", 11), ("randband_20k", 2000), ("geoknn_1m", 3000)])
 def test_k3_layouts_bitwise_equal(env, name, n, monkeypatch):
     """K3 has two layouts (k3_smem.cu): the thread-major ELL (K3E, rows <= 16 entries) and the CSR
