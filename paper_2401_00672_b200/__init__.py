@@ -14,7 +14,7 @@ import numpy as np
 from . import _lib as L
 from ._lib import PobkError, Report, KERNEL, STOP, TERM_NAME  # noqa: F401
 
-__all__ = ["Plan", "PobkError", "Report", "solve_batch", "KERNEL", "STOP"]
+__all__ = ["Plan", "PobkError", "Report", "solve_batch", "lane_tile_rows", "half_gpu_tile_rows", "KERNEL", "STOP"]
 
 
 def _torch():
@@ -178,9 +178,16 @@ def solve_batch(plans, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int 
     return list(reps)
 
 
-def half_gpu_tile_rows(m: int, device: int | None = None) -> int:
-    """tile_rows for a K2 plan whose tiles fill at most half of the device's SMs (batched solves
-    then run two systems concurrently, pobk_solve_batch)."""
+def lane_tile_rows(m: int, lanes: int = 2, device: int | None = None) -> int:
+    """tile_rows for a K2 plan whose tiles fill at most 1/lanes of the device's SMs, so that
+    pobk_solve_batch runs `lanes` systems (or right-hand sides of one matrix, one plan each)
+    side by side.  The tiles must still keep their columns in shared memory: 2 lanes suit the 1M-row
+    configs, 4 lanes the 262k-row config 3."""
     import torch
     sms = torch.cuda.get_device_properties(device if device is not None else torch.cuda.current_device()).multi_processor_count
-    return -(-int(m) // max(1, sms // 2 - 2))
+    return -(-int(m) // max(1, sms // max(1, int(lanes)) - 2))
+
+
+def half_gpu_tile_rows(m: int, device: int | None = None) -> int:
+    """lane_tile_rows(m, 2): tiles filling at most half of the device's SMs (two lanes)."""
+    return lane_tile_rows(m, 2, device)

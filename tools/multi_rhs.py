@@ -3,7 +3,7 @@ plan per right-hand side (the matrix's preprocessing is shared on the host: perm
 bitwise the same), half-GPU K2 tilings so two solves run side by side.  Compares with back-to-back
 full-GPU solves; results must be bitwise equal (development/reporting aid).
 
-    python tools/multi_rhs.py [config] [R]
+    python tools/multi_rhs.py [config] [R] [lanes]
 """
 import sys, time, json
 import numpy as np, torch
@@ -22,8 +22,10 @@ fs = [torch.from_numpy(A @ xs).cuda() for xs in xstars]
 xss = [torch.from_numpy(xs).cuda() for xs in xstars]
 tol = TOL[name]
 res = {}
+nl = int(sys.argv[3]) if len(sys.argv) > 3 else 2  # lanes (tiles per system: SMs / nl)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
 for mode in ("back-to-back", "lanes"):
-    tr = 0 if mode == "back-to-back" else pk.half_gpu_tile_rows(s.m)
+    tr = 0 if mode == "back-to-back" else -(-s.m // max(1, sms // nl - 2))
     plans = [pk.Plan.from_system(s, tile_rows=tr) for _ in range(R)]
     xs = [torch.zeros(s.m, dtype=torch.float64, device="cuda") for _ in range(R)]
     for it in range(3):
