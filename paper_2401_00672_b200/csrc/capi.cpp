@@ -131,14 +131,14 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
     if (!k3ok) return fail(POBK_ERR_ARG, "kernel=SMEM requested but the system needs " + std::to_string(k3b) + " B of shared memory");
   } else if (req == POBK_KERNEL_WAVEFRONT) {
     if (p.any_overlap) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT does not support overlapping categories (thr > 0)");
-    if (!k2_build(p, At, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
+    if (!k2_build(p, At, nrm2, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
   } else if (req == POBK_KERNEL_CLUSTER) {
     if (!k4_build(p, rp, col, val, why)) return fail(POBK_ERR_ARG, "kernel=CLUSTER unavailable: " + why);
   } else if (req == POBK_KERNEL_AUTO) {
     // K3 (one CTA) when the system fits one CTA's shared memory, else the K2 wavefront from
     // m >= 4096, else K1 (K4, one cluster, is explicit-only: slower than K2 where both apply)
     if (k3ok) p.kernel = POBK_KERNEL_SMEM;
-    else if (!p.any_overlap && m >= 4096 && k2_build(p, At, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
+    else if (!p.any_overlap && m >= 4096 && k2_build(p, At, nrm2, tile_rows, why)) p.kernel = POBK_KERNEL_WAVEFRONT;
     else p.kernel = POBK_KERNEL_LAUNCH;
   }
   return POBK_OK;

@@ -49,6 +49,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <mutex>
 #include <set>
 #include <string>
 #include <vector>
@@ -80,13 +81,15 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15LL); }
 
-// slice block (bytes): val[W*R] f[R] (fp64) | col[W*R] (u32: shared flag | index)
+// slice block (bytes): val[W*R] f[R] (fp64) | [boundary slices] n2[R] (fp64: ||a~||^2)
+//                      | col[W*R] (u32: shared flag | index)
 //                      | [boundary slices] mout[W*R] (u32: wrap flag | mailbox index) | len[R] (u16)
 struct SliceLayout {
-  int o_f, o_col, o_mout, o_len, bytes;
+  int o_f, o_n2, o_col, o_mout, o_len, bytes;
   __host__ __device__ SliceLayout(int R, int W, bool bnd) {
     o_f = 8 * W * R;
-    o_col = o_f + 8 * R;
+    o_n2 = o_f + 8 * R;
+    o_col = o_n2 + (bnd ? 8 * R : 0);
     o_mout = o_col + 4 * W * R;
     o_len = o_mout + (bnd ? 4 * W * R : 0);
     bytes = a16(o_len + 2 * R);
@@ -125,6 +128,9 @@ struct K2Args {
   int nsl_max, nck_max, ntask_max, np_max;  // shared-memory sizing
   unsigned long long* trace;  // optional [T*ntask_max*12] globaltimer stamps of one sweep (POBK_K2_TRACE=s)
   int trace_sweep;
+  int nap;                    // vector boundary slices: mailbox poll back-off (ns)
+  int strict;                 // strict boundary priority (barrier 3 after every boundary post)
+  int ireg;                   // register-resident interior slices (256-thread instantiation)
 };
 
 // shared-memory control block
@@ -554,44 +560,49 @@ __device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, d
       : "r"(p0), "r"(p1), "r"(p2), "r"(p3), "r"(a0), "r"(a1), "r"(a2), "r"(a3));
 }
 
-// Register-resident boundary slice (the 256-thread instantiation): the row's columns, values and
-// ||a~||^2 are loaded from the ring BEFORE the barrier that closes the tile's previous task,
-// together with the mailbox poll; after the barrier only the private x~ loads (all in flight at
-// once), the row sum, the division and the write-back remain on the critical path.  Same
-// arithmetic in the same order as BSlice (the common.cuh contract).
+// Register-resident boundary slice (the 256-thread instantiation): the row's values, one target
+// word per entry (a private entry's x~ address in shared memory, a shared entry's mailbox target)
+// and ||a~||^2 (from the stream: the host's left-to-right sum, the oracle's O1 order) are loaded
+// from the ring BEFORE the barrier that closes the tile's previous task, together with the
+// mailbox poll; after the barrier only the private x~ loads (all in flight at once), the row
+// sum, the division and the stores remain on the critical path.  Same arithmetic in the same
+// order as BSlice (the common.cuh contract).
 struct BSlice2 {
   double xr[kMaxJ];
   double av[kMaxJ];
-  unsigned cr[kMaxJ];
-  unsigned shm;
+  unsigned tg[kMaxJ];
+  unsigned shm, prv;  // bit j: entry j is a real shared entry / a private entry (incl. ELL padding)
   double n2;
-  __device__ __forceinline__ void pre(const SliceAddr& S, int W) {
+  __device__ __forceinline__ void pre(const SliceAddr& S, int W, int R, int lane, unsigned blk, unsigned xb) {
     shm = 0u;
-    n2 = 0.0;
+    prv = 0u;
+    {
+      const SliceLayout Ly(R, W, true);
+      n2 = lds64(blk + (unsigned)Ly.o_n2 + 8u * (lane < R ? lane : 0));
+    }
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
       if (jb < W) {
-        unsigned ad[kBatch], c8[kBatch];
+        unsigned ad[kBatch], c8[kBatch], m8[kBatch];
         double a8[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
         lds32x8(c8, ad);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) ad[u] = S.mb + min(jb + u, W - 1) * S.cs;
+        lds32x8(m8, ad);
 #pragma unroll
         for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
         lds64x8(a8, ad);
 #pragma unroll
         for (int u = 0; u < kBatch; u++) {
           const int j = jb + u;
-          cr[j] = c8[u];
           av[j] = j < W ? a8[u] : 0.0;
-          const bool sh = (c8[u] & kShared) && j < S.myl;
-          shm |= sh ? (1u << j) : 0u;
+          const bool sh = (c8[u] & kShared) != 0u;
+          shm |= (sh && j < S.myl) ? (1u << j) : 0u;
+          prv |= (!sh && j < W) ? (1u << j) : 0u;
+          tg[j] = sh ? m8[u] : xb + 8u * (c8[u] & kIdx);
         }
-        double qq[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) qq[u] = pin(__dmul_rn(av[jb + u], av[jb + u]));
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) n2 = __dadd_rn(n2, qq[u]);  // left to right, as the oracle
       }
     }
   }
@@ -606,18 +617,12 @@ struct BSlice2 {
       for (int j = 0; j < kMaxJ; j++)
         if ((pend >> j) & 1u) np |= ((unsigned long long)__double_as_longlong(xr[j]) == kSentinel) ? (1u << j) : 0u;
       pend = np;
-      if (kAbl & 1) {  // ablation: no wait (an empty slot reads as +0, not as the NaN sentinel)
-#pragma unroll
-        for (int j = 0; j < kMaxJ; j++)
-          if ((pend >> j) & 1u) xr[j] = 0.0;
-        break;
-      }
       if (!__any_sync(kFull, pend != 0u)) break;
       if (POBK_K2_POLLSLEEP) __nanosleep(POBK_K2_POLLSLEEP);
     }
 #pragma unroll
     for (int j4 = 0; j4 < kMaxJ; j4 += 4)
-      if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
+      if (j4 < W) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
                                        unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
@@ -629,15 +634,9 @@ struct BSlice2 {
       if ((j & ~(kBatch - 1)) < W) xr[j] = ((shm >> j) & 1u) ? xr[j] : 0.0;
 #pragma unroll
     for (int j4 = 0; j4 < kMaxJ; j4 += 4) {
-      if (j4 < W) {
-        unsigned p[4], ad[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          p[u] = (j4 + u < W && !(cr[j4 + u] & kShared)) ? 1u : 0u;
-          ad[u] = xb + 8u * (cr[j4 + u] & kIdx);
-        }
-        lds64x4_if(xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3], p[0], p[1], p[2], p[3], ad[0], ad[1], ad[2], ad[3]);
-      }
+      if (j4 < W)
+        lds64x4_if(xr[j4], xr[j4 + 1], xr[j4 + 2], xr[j4 + 3], (prv >> j4) & 1u, (prv >> (j4 + 1)) & 1u, (prv >> (j4 + 2)) & 1u,
+                   (prv >> (j4 + 3)) & 1u, tg[j4], tg[j4 + 1], tg[j4 + 2], tg[j4 + 3]);
     }
 #if POBK_K2_PRIO
     if (prio) {  // operands in registers: let the interior warps at the shared-memory pipe
@@ -662,7 +661,6 @@ struct BSlice2 {
         for (int u = 0; u < kBatch; u++) s = __dadd_rn(s, pp[u]);
       }
     }
-    double n2t = n2;
     for (int j = kMaxJ; j < W; j++) {  // long rows: entries past the register window
       const unsigned cj = lds32(S.cb + j * S.cs);
       const double a = lds64(S.vb + j * S.vs);
@@ -677,7 +675,6 @@ struct BSlice2 {
         x = lds64(xb + 8u * (cj & kIdx));
       }
       s = __dadd_rn(s, __dmul_rn(a, x));
-      n2t = __dadd_rn(n2t, __dmul_rn(a, a));
     }
     if (trp) {
       double s2 = s;
@@ -685,7 +682,7 @@ struct BSlice2 {
       __syncwarp();
       if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
     }
-    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2t);
+    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
     if (trp) {
       double a2 = alpha;
       asm volatile("mov.b64 %0, %0;" : "+d"(a2));
@@ -700,19 +697,12 @@ struct BSlice2 {
       if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
     }
 #pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // write back: a batch of mailbox targets, then its stores
-      if (jb < W) {
-        unsigned mo[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) mo[u] = lds32(S.mb + min(jb + u, W - 1) * S.cs);
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {
-          const int j = jb + u;
-          const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
-          if (!(kAbl & 32)) sts64_if(act & (sh ^ 1u), xb + 8u * (cr[j] & kIdx), xr[j]);
-          stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
-                 (unsigned long long)__double_as_longlong(xr[j]));
-        }
+    for (int j = 0; j < kMaxJ; j++) {  // write back: the targets are in registers (pre)
+      if ((j & ~(kBatch - 1)) < W) {
+        const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
+        sts64_if(act & (sh ^ 1u), tg[j], xr[j]);
+        stm_if(act & sh, mbox + ((tg[j] & ~kWrap) + ((tg[j] & kWrap) ? off_q : off_p)),
+               (unsigned long long)__double_as_longlong(xr[j]));
       }
     }
     for (int j = kMaxJ; j < W; j++) {  // tail: the slot still holds the consumed value (re-armed now)
@@ -732,7 +722,258 @@ struct BSlice2 {
     if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
-template <int kNT, bool kBReg>
+// Vector boundary slice ("lane-parallel boundary rows"): R rows x L lanes
+// (R*L = RL <= 32); entry j of row r sits at lane r*L + j%L of round q = j/L, so the x~ loads,
+// products, new values and write-back of one row are spread over L lanes (Q = ceil(W/L) rounds
+// each).  The row sum still runs in the oracle's order (common.cuh): each lane writes its products
+// back over its own values in the slice's ring slot, and every lane of the row's group reads the
+// row's products in entry order (16-byte pairs) and forms the same left-to-right chain, so the
+// group agrees on alpha with no broadcast -- bit for bit the one-lane result.  ||a~||^2 comes
+// from the stream (computed on the host in the same left-to-right order).  A lane's mailbox
+// slots are contiguous (round q at lane*Qp + q, Qp = Q rounded up to 4): one 256-bit poll load
+// per four rounds.
+//   stream block: val[Q*RL] (fp64) | f[R] | n2[R] (fp64) | col[Q*RL] (u32) | mout[Q*RL] (u32) | len[R] (u16)
+struct VLayout {
+  int Q, o_f, o_n2, o_col, o_mout, o_len, bytes;
+  __host__ __device__ VLayout(int R, int L, int W) {
+    Q = (W + L - 1) / L;
+    const int n = Q * R * L;
+    o_f = 8 * n;
+    o_n2 = o_f + 8 * R;
+    o_col = o_n2 + 8 * R;
+    o_mout = o_col + 4 * n;
+    o_len = o_mout + 4 * n;
+    bytes = a16(o_len + 2 * R);
+  }
+};
+__host__ __device__ constexpr int vslice_qmax(int L) { return L >= 8 ? 4 : 8; }  // rounds in registers: W <= qmax * L
+
+// predicated shared-memory access helpers for the vector slices (registers keep their value, or
+// nothing is stored, where the predicate is off; no branches)
+__device__ __forceinline__ void lds64_if(double& v, unsigned p, unsigned a) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.shared.f64 %0, [%2];\n}" : "+d"(v) : "r"(p), "r"(a));
+}
+__device__ __forceinline__ void lds128_if(double& x, double& y, unsigned p, unsigned a) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%3];\n}"
+               : "+d"(x), "+d"(y)
+               : "r"(p), "r"(a));
+}
+__device__ __forceinline__ unsigned lds32_if(unsigned p, unsigned a) {
+  unsigned v = 0u;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.shared.u32 %0, [%2];\n}" : "+r"(v) : "r"(p), "r"(a));
+  return v;
+}
+
+template <int L>
+struct VSlice {
+  static constexpr int kQ = vslice_qmax(L);
+  double xr[kQ], av[kQ];
+  unsigned tg[kQ];    // round q: private entry -> shared-window address of its x~; shared -> mailbox target
+  unsigned shm, prv;  // bit q: this lane's round-q entry is a real shared / a real private entry
+  double n2, f;
+  int Q, RL;
+  unsigned vq, pb;    // (live lanes) shared-window address of this lane's val entry 0; of its row's entry 0
+  // operands from the ring (before the barrier that closes the tile's previous task)
+  __device__ __forceinline__ void pre(unsigned blk, int R, int W, int lane, unsigned xb) {
+    RL = R * L;
+    const VLayout V(R, L, W);
+    Q = V.Q;
+    const bool live = lane < RL;
+    const int ln = live ? lane : 0, r = ln / L, l = ln - r * L;
+    vq = live ? blk + 8u * ln : 0u;
+    pb = blk + 8u * (r * L);
+    f = lds64(blk + (unsigned)V.o_f + 8u * r);
+    n2 = lds64(blk + (unsigned)V.o_n2 + 8u * r);
+    const int len = live ? (int)lds16(blk + (unsigned)V.o_len + 2u * r) : 0;
+    unsigned c[kQ], mo[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; q++) {
+      const unsigned in = q < Q ? 1u : 0u, e = (unsigned)((q < Q ? q : 0) * RL + ln);
+      c[q] = lds32_if(in, blk + (unsigned)V.o_col + 4u * e);
+      mo[q] = lds32_if(in, blk + (unsigned)V.o_mout + 4u * e);
+      av[q] = 0.0;
+      lds64_if(av[q], in & (live ? 1u : 0u), blk + 8u * e);  // (ELL padding: value +0)
+    }
+    shm = 0u;
+    prv = 0u;
+#pragma unroll
+    for (int q = 0; q < kQ; q++) {
+      const bool real = live && q < Q && q * L + l < len, sh = (c[q] & kShared) != 0u;
+      shm |= (real && sh) ? (1u << q) : 0u;
+      prv |= (real && !sh) ? (1u << q) : 0u;
+      tg[q] = sh ? mo[q] : xb + 8u * (c[q] & kIdx);
+      xr[q] = 0.0;
+    }
+  }
+  // this lane's slots: mbox_in[q], q < Q (contiguous, 32-byte aligned), polled until no sentinel
+  __device__ __forceinline__ void poll(unsigned long long* mbox_in, int nap) {
+    unsigned pend = shm;
+    double t[kQ];
+    for (int it = 0;; it++) {
+      if (it > 0 && nap > 0) __nanosleep(nap);  // back-off: spinning warps crowd the load/store unit
+#pragma unroll
+      for (int q4 = 0; q4 < kQ; q4 += 4) ldm4_if((pend >> q4) & 0xFu, mbox_in + q4, t[q4], t[q4 + 1], t[q4 + 2], t[q4 + 3]);
+      unsigned np = 0u;
+#pragma unroll
+      for (int q = 0; q < kQ; q++) {
+        const bool pq = (pend >> q) & 1u, empty = (unsigned long long)__double_as_longlong(t[q]) == kSentinel;
+        np |= (pq && empty) ? (1u << q) : 0u;
+        xr[q] = (pq && !empty) ? t[q] : xr[q];
+      }
+      pend = np;
+      if (!__any_sync(kFull, pend != 0u)) break;
+    }
+#pragma unroll
+    for (int q4 = 0; q4 < kQ; q4 += 4) stm4_if((shm >> q4) & 0xFu, mbox_in + q4, kSentinel);  // re-armed for the sweep after next
+  }
+  __device__ __forceinline__ void post(unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
+                                       int prio) {
+    // private x~ (final once the tile's previous task is done), all in flight at once
+#pragma unroll
+    for (int q = 0; q < kQ; q++) lds64_if(xr[q], (prv >> q) & 1u, tg[q]);
+#if POBK_K2_PRIO
+    if (prio) {
+#pragma unroll
+      for (int q = 0; q < kQ; q++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[q]));
+      named_arrive(3, prio);
+    }
+#endif
+    if (POBK_K2_FT && trp) {  // all private x~ loads complete
+#pragma unroll
+      for (int q = 0; q < kQ; q++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[q]));
+      if ((threadIdx.x & 31) == 0) trp[11] = gtimer();
+    }
+    // each lane's products over its own values in the ring slot (every lane read its values in
+    // pre), then the row's products in entry order, 16-byte pairs, loaded two rounds ahead of the
+    // left-to-right chain (padding products are +0: adding them is exact)
+#pragma unroll
+    for (int q = 0; q < kQ; q++) sts64_if(vq != 0u && q < Q, vq + 8u * (unsigned)(q * RL), __dmul_rn(av[q], xr[q]));
+    __syncwarp();
+    double pr[kQ][L];
+#pragma unroll
+    for (int q = 0; q < kQ; q++)
+#pragma unroll
+      for (int u = 0; u < L; u++) pr[q][u] = 0.0;
+    constexpr int kAhead = 2;
+#pragma unroll
+    for (int q = 0; q < kAhead && q < kQ; q++)
+#pragma unroll
+      for (int u = 0; u < L; u += 2) lds128_if(pr[q][u], pr[q][u + 1], q < Q, pb + 8u * (unsigned)(q * RL + u));
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQ; q++) {
+      if (q + kAhead < kQ) {
+#pragma unroll
+        for (int u = 0; u < L; u += 2)
+          lds128_if(pr[q + kAhead][u], pr[q + kAhead][u + 1], q + kAhead < Q, pb + 8u * (unsigned)((q + kAhead) * RL + u));
+      }
+      if (q < Q) {
+#pragma unroll
+        for (int u = 0; u < L; u++) s = __dadd_rn(s, pr[q][u]);
+      }
+    }
+    if (trp) {
+      double s2 = s;
+      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
+    }
+    const double alpha = __ddiv_rn(__dsub_rn(f, s), n2);
+    if (trp) {
+      double a2 = alpha;
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) trp[9] = gtimer();
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; q++) xr[q] = __dadd_rn(xr[q], __dmul_rn(alpha, av[q]));
+    if (POBK_K2_FT && trp) {
+      double a2 = xr[0];
+      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
+      if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; q++) {
+      sts64_if((prv >> q) & 1u, tg[q], xr[q]);
+      stm_if((shm >> q) & 1u, mbox + ((tg[q] & ~kWrap) + ((tg[q] & kWrap) ? off_q : off_p)),
+             (unsigned long long)__double_as_longlong(xr[q]));
+    }
+    if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
+  }
+};
+
+// interior slice, register-resident x~ (256-thread instantiation, W <= kMaxJ): columns, then the
+// x~ they address, all in flight together and kept in registers; values are read once per pass.
+// Entries past the slice width are not read at all (slice_interior reads columns, values and x~
+// in both passes, padded to batches of 8).  Same operations in the same order (common.cuh).
+__device__ __forceinline__ void slice_interior_reg(const SliceAddr& S, int W, unsigned xb) {
+  unsigned c[kMaxJ];
+  double xv[kMaxJ];
+#pragma unroll
+  for (int j = 0; j < kMaxJ; j++) c[j] = lds32_if(j < W ? 1u : 0u, S.cb + (unsigned)j * S.cs);
+#pragma unroll
+  for (int j = 0; j < kMaxJ; j++) {
+    xv[j] = 0.0;
+    lds64_if(xv[j], j < W ? 1u : 0u, xb + 8u * c[j]);
+  }
+  double s = 0.0, n2 = 0.0;
+#pragma unroll
+  for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+    if (jb < W) {  // entries past the width are +0 * +0: bit-exact no-ops
+      double av[kBatch], pp[kBatch], qq[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        av[u] = 0.0;
+        lds64_if(av[u], jb + u < W ? 1u : 0u, S.vb + (unsigned)(jb + u) * S.vs);
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        pp[u] = pin(__dmul_rn(av[u], xv[jb + u]));
+        qq[u] = pin(__dmul_rn(av[u], av[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        s = __dadd_rn(s, pp[u]);
+        n2 = __dadd_rn(n2, qq[u]);
+      }
+    }
+  }
+  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+#pragma unroll
+  for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+    if (jb < W) {
+      double av[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; u++) {
+        av[u] = 0.0;
+        lds64_if(av[u], jb + u < W ? 1u : 0u, S.vb + (unsigned)(jb + u) * S.vs);
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; u++)
+        sts64_if(jb + u < S.myl ? 1u : 0u, xb + 8u * c[jb + u], __dadd_rn(xv[jb + u], __dmul_rn(alpha, av[u])));
+    }
+  }
+}
+
+// one vector boundary slice of lane width L: pre, poll, [barrier], post
+template <int L>
+__device__ __forceinline__ void run_vslice(unsigned blk, int R, int W, int lane, unsigned long long* mbox_s, bool bar,
+                                           int nc, unsigned xb, unsigned long long* mbox, unsigned off_p, unsigned off_q,
+                                           unsigned long long* trp, int prio, int nap) {
+  VSlice<L> V;
+  V.pre(blk, R, W, lane, xb);
+  if (trp && lane == 0) trp[8] = gtimer();
+  V.poll(mbox_s + (size_t)(lane < V.RL ? lane : 0) * ((V.Q + 3) & ~3), nap);
+  if (trp && lane == 0) trp[1] = gtimer();
+  if (bar) named_bar(1, nc);
+  if (trp && lane == 0) trp[3] = gtimer();
+  V.post(mbox, off_p, off_q, trp, prio);
+}
+
+// kVL: lane width of the plan's vector boundary slices (0: none); kIReg: register-resident
+// interior slices.  One instantiation per plan shape keeps each kernel's register allocation
+// to the paths it runs (every path inlined into one kernel spilled and ran 2x slower).
+template <int kNT, bool kBReg, int kVL, bool kIReg>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
@@ -859,12 +1100,20 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
 #if POBK_K2_PRIO
         // boundary priority: the interior warps start the task once the look-ahead warps hold
         // their private operands (barrier 3: look-ahead warps arrive, the others sync)
-        if (kBReg && !la) named_bar(3, kNC);
+        if (kBReg && !la && !a.strict) named_bar(3, kNC);
 #endif
+        // strict boundary priority (a.strict): no interior slice of the task starts before every
+        // boundary slice of the task is posted (barrier 3, every compute warp once per task), so
+        // the boundary rows' shared-memory round trips do not queue behind the interior's traffic
+        bool bdone = !a.strict;
         for (int q = qs; q < qe; q += qstep) {
           const bool bnd = q < nbnd;
+          if (!bnd && !bdone) {
+            named_bar(3, kNC);
+            bdone = true;
+          }
           const int4 sl = smeta[tm.x + q];
-          const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
+          const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z & 0xffff, VL = sl.z >> 16;
           const unsigned long long g = (unsigned long long)sweep * nck + chunk;
           // ring position of chunk g without 64-bit division: h = g mod 2NS from the sweep's base
           // and the chunk's residue (precomputed); slot = h mod NS, phase parity = h >= NS
@@ -876,6 +1125,21 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
           const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
+          if (kVL > 0 && bnd && VL) {  // vector boundary slice (L lanes per row)
+            unsigned long long* const mbox_s = mbox_p + sl.w;
+            const bool bar = la && q == qs && ti > 0 && !(kAbl & 2);
+            const int prio = (kBReg && la && q == qs && !a.strict) ? kNC : 0;
+            unsigned long long* const vtr = (tr && q == 0) ? trp : nullptr;
+            if constexpr (kVL > 0) run_vslice<kVL>(blk, R, W, lane, mbox_s, bar, kNC, xb, a.mbox, off_p, off_q, vtr, prio, a.nap);
+            if (vtr) {
+              __syncwarp();
+              if (lane == 0) trp[10] = gtimer();
+            }
+            __syncwarp();
+            if (lane == 0) atomicAdd(&ctl->released[slot], 1);
+            if (tr && lane == 0 && q == 0) trp[5] = gtimer();
+            continue;
+          }
           const SliceAddr S(blk, R, W, bnd, lane);
           if (kAbl & 16) {
             if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
@@ -884,7 +1148,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             const bool bar = la && q == qs && ti > 0 && !(kAbl & 2);  // look-ahead slice: barrier after the poll
             if constexpr (kBReg) {
               BSlice2 B;
-              B.pre(S, W);
+              B.pre(S, W, R, lane, blk, xb);
               if (tr && q == 0 && lane == 0) trp[8] = gtimer();
               B.poll(W, mbox_in);
               if (tr && q == 0 && lane == 0) trp[1] = gtimer();
@@ -892,7 +1156,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (bar) named_bar(1, kNC);
               if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs) ? kNC : 0);
+              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs && !a.strict) ? kNC : 0);
             } else {
               BSlice B;
               B.pre(S, W, xb);
@@ -910,12 +1174,14 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (lane == 0) trp[10] = gtimer();
             }
           } else if (!(kAbl & 4)) {
-            slice_interior(S, W, xb);
+            if (kIReg && W <= kMaxJ) slice_interior_reg(S, W, xb);
+            else slice_interior(S, W, xb);
           }
           __syncwarp();
           if (lane == 0) atomicAdd(&ctl->released[slot], 1);
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 5 : 7] = gtimer();
         }
+        if (!bdone) named_bar(3, kNC);
       }
       named_bar(1, kNC);  // the sweep's last task is complete
       sweep++;
@@ -1074,6 +1340,7 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 struct K2Plan {
   int T = 0, NS = 0;
   int nt = 256;                // threads per CTA: 256 (BSlice2) or 512 (BSlice), see k2_build
+  int vl = 0;                  // lane width of the vector boundary slices (0: one lane per row)
   size_t smem = 0;
   int nsl_max = 1, nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
@@ -1200,7 +1467,7 @@ double private_fraction(const HostCSR& A, const std::vector<int32_t>& tile) {
 }
 }  // namespace
 
-bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
+bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why) {
   if (p.any_overlap) { why = "overlapping categories"; return false; }
   int sms = 148;
   cudaDeviceProp prop;
@@ -1302,6 +1569,46 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       rows_tk[tile[r]][k].push_back(r);
     }
   auto rlen = [&](int32_t r) { return (int)(At.ptr[r + 1] - At.ptr[r]); };
+  // CTA size (see the upload below): from the one-lane slicing's slices per task
+  int nt_choice = 256;
+  {
+    long long ns = 0, ntk = 0;
+    for (int t = 0; t < T; t++)
+      for (int k = 0; k < p.nsteps; k++) {
+        if (rows_tk[t][k].empty()) continue;
+        int nb = 0;
+        for (int32_t r : rows_tk[t][k]) nb += boundary[r];
+        const int ni = (int)rows_tk[t][k].size() - nb;
+        ns += (nb + kSliceRows - 1) / kSliceRows + (ni + kSliceRows - 1) / kSliceRows;
+        ntk++;
+      }
+    nt_choice = (double)ns / std::max<long long>(ntk, 1) > 10.0 ? 512 : 256;
+    if (const char* e = getenv("POBK_K2_THREADS")) nt_choice = atoi(e) == 512 ? 512 : 256;  // development override
+  }
+  // boundary rows as vector slices of L lanes per row, one width per plan (0: one lane per row):
+  // 8 when the median task's boundary rows fit one 4-row slice per compute warp, else 4
+  int vl_plan = 0;
+  {
+    std::vector<int> nbr;
+    for (int t = 0; t < T; t++)
+      for (int k = 0; k < p.nsteps; k++) {
+        int nb = 0;
+        for (int32_t r : rows_tk[t][k]) nb += boundary[r];
+        if (nb) nbr.push_back(nb);
+      }
+    if (!nbr.empty() && getenv("POBK_K2_VL")) {  // (opt-in: slower than one lane per row so far)
+      std::nth_element(nbr.begin(), nbr.begin() + nbr.size() / 2, nbr.end());
+      const int nwc = nt_choice / 32 - 1, med = nbr[nbr.size() / 2];
+      vl_plan = (nt_choice == 512 || med <= 4 * nwc) ? 8 : 4;
+    }
+    if (const char* e = getenv("POBK_K2_VL")) {  // development override: 0, 4 or 8
+      const int v = atoi(e);
+      vl_plan = v == 0 ? 0 : (v == 4 && nt_choice == 256) ? 4 : 8;
+    }
+  }
+  std::vector<int64_t> mb_base(m, -1);  // boundary rows: mailbox base of their slice
+  std::vector<int16_t> mb_L(m, 0), mb_r(m, 0);
+  std::vector<int32_t> mb_RL(m, 0);  // (vector slices: slots per lane, Qp)
   std::vector<int4> smeta, cmeta, tmeta;
   std::vector<int> tile_slice(T + 1, 0), tile_chunk(T + 1, 0), tile_task(T + 1, 0);
   std::vector<std::vector<int32_t>> slice_rows;  // global slice order
@@ -1327,9 +1634,15 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
         size_t a = 0;
         while (a < g.size()) {
           const int W = rlen(g[a]);
+          // a vector slice of 32/VL rows, or (rows past the register rounds) a one-lane slice
+          const int VL = (bnd && vl_plan && W <= vslice_qmax(vl_plan) * vl_plan) ? vl_plan : 0;
           size_t b = a;
-          while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
-          const int R = (int)(b - a), bytes = SliceLayout(R, W, bnd).bytes;
+          if (VL) {
+            b = std::min(g.size(), a + (size_t)(32 / VL));
+          } else {
+            while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
+          }
+          const int R = (int)(b - a), bytes = VL ? VLayout(R, VL, W).bytes : SliceLayout(R, W, bnd).bytes;
           for (size_t r = a; r < b; r++) pad += W - rlen(g[r]);
           if (chunk_bytes + bytes > kSlot) {  // open a new chunk
             chunk_local++;
@@ -1338,14 +1651,26 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
           }
           if (chunk_local >= (1 << 20)) { why = "too many chunks in tile " + std::to_string(t); return false; }
           int mbase = 0;
-          if (bnd) {
+          if (bnd && VL) {  // round q of lane r*VL + l: slot mbase + (r*VL + l)*Qp + q
+            const int Qp = ((W + VL - 1) / VL + 3) & ~3;
+            const long long n = (long long)Qp * R * VL;
+            if (2 * (NB + n) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
+            mbase = (int)NB;
+            for (int r = 0; r < R; r++) {
+              mb_base[g[a + r]] = NB;
+              mb_L[g[a + r]] = (int16_t)VL;
+              mb_RL[g[a + r]] = Qp;
+              mb_r[g[a + r]] = (int16_t)r;
+            }
+            NB += n;
+          } else if (bnd) {
             const int Wp = (W + 3) & ~3;  // a lane's slots: contiguous, 32-byte aligned groups of 4
-            if (2 * (NB + (long long)Wp * R) >= (1LL << 32)) { why = "too many boundary entries for the mailboxes"; return false; }
+            if (2 * (NB + (long long)Wp * R) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
             mbase = (int)NB;
             for (int r = 0; r < R; r++) mb_of_row[g[a + r]] = NB + (long long)r * Wp;
             NB += (long long)Wp * R;
           }
-          smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W, mbase));
+          smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W | (VL << 16), mbase));
           slice_rows.emplace_back(g.begin() + a, g.begin() + b);
           slice_pos.push_back(off);
           slice_bnd.push_back(bnd);
@@ -1395,7 +1720,21 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
       // wavefront), so an access group is (slice, entry j, half)
       for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
         const auto& rows = slice_rows[si];
-        const int W = smeta[si].z;
+        const int W = smeta[si].z & 0xffff, VL = smeta[si].z >> 16;
+        if (VL) {  // vector slice: round q is one warp access, lane r*VL + j%VL
+          const int Q = (W + VL - 1) / VL;
+          for (int q = 0; q < Q; q++, ng += 2)
+            for (size_t r = 0; r < rows.size(); r++)
+              for (int l = 0; l < VL; l++) {
+                const int32_t i = rows[r];
+                const int j = q * VL + l;
+                if (j < rlen(i)) {
+                  const int32_t cg = At.col[At.ptr[i] + j];
+                  if (!shared[cg]) groups_of[local[cg]].push_back(ng + ((int)r * VL + l >= 16 ? 1 : 0));
+                }
+              }
+          continue;
+        }
         for (int j = 0; j < W; j++, ng += 2)
           for (size_t r = 0; r < rows.size(); r++) {
             const int32_t i = rows[r];
@@ -1488,9 +1827,11 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
     std::vector<int32_t> row_of_entry(At.nnz());
     for (int64_t i = 0; i < m; i++)
       for (int64_t q = At.ptr[i]; q < At.ptr[i + 1]; q++) row_of_entry[q] = (int32_t)i;
-    auto slot_of = [&](int64_t q) {  // mailbox slot of CSR entry q (its row is a boundary row)
+    auto slot_of = [&](int64_t q) -> int64_t {  // mailbox slot of CSR entry q (its row is a boundary row)
       const int32_t i = row_of_entry[q];
-      return mb_of_row[i] + (q - At.ptr[i]);
+      const int64_t j = q - At.ptr[i];
+      if (mb_L[i]) return mb_base[i] + ((int64_t)mb_r[i] * mb_L[i] + j % mb_L[i]) * mb_RL[i] + j / mb_L[i];
+      return mb_of_row[i] + j;
     };
     std::vector<std::vector<std::pair<int, int>>> per(T);
     std::vector<int64_t> ch;
@@ -1521,10 +1862,43 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   fslot.reserve(m);
   for (size_t si = 0; si < slice_rows.size(); si++) {
     const auto& rows = slice_rows[si];
-    const int R = (int)rows.size(), W = smeta[si].z;
+    const int R = (int)rows.size(), W = smeta[si].z & 0xffff, VL = smeta[si].z >> 16;
     const bool bnd = slice_bnd[si];
-    const SliceLayout L(R, W, bnd);
     unsigned char* blk = stream.data() + slice_pos[si];
+    if (VL) {  // vector slice (VSlice): entry j of row r at round j/VL, lane r*VL + j%VL
+      const VLayout V(R, VL, W);
+      const int Q = (W + VL - 1) / VL, RL = R * VL;
+      double* val = (double*)blk;
+      double* fv = (double*)(blk + V.o_f);
+      double* n2v = (double*)(blk + V.o_n2);
+      unsigned* col = (unsigned*)(blk + V.o_col);
+      unsigned* mout = (unsigned*)(blk + V.o_mout);
+      unsigned short* len = (unsigned short*)(blk + V.o_len);
+      for (int r = 0; r < R; r++) {
+        const int32_t i = rows[r];
+        for (int j = 0; j < Q * VL; j++) {
+          const int e = (j / VL) * RL + r * VL + j % VL;
+          if (j < rlen(i)) {
+            const int64_t q = At.ptr[i] + j;
+            const int32_t cg = At.col[q];
+            col[e] = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
+            val[e] = At.val[q];
+            mout[e] = shared[cg] ? mout_of_entry[q] : 0u;
+          } else {
+            col[e] = (unsigned)np_max;  // ELL padding: zero slot, value +0 (never stored: len)
+            val[e] = 0.0;
+            mout[e] = 0u;
+          }
+        }
+        len[r] = (unsigned short)rlen(i);
+        fv[r] = 0.0;
+        n2v[r] = nrm2[i];  // ||a~_i||^2, left to right from 0 (row_sqnorms: the oracle's O1 order)
+        orig_q.push_back(p.perm[i]);
+        fslot.push_back((slice_pos[si] + V.o_f) / 8 + r);
+      }
+      continue;
+    }
+    const SliceLayout L(R, W, bnd);
     double* val = (double*)blk;
     double* fv = (double*)(blk + L.o_f);
     unsigned* col = (unsigned*)(blk + L.o_col);
@@ -1540,6 +1914,7 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
         if (bnd) mout[j * R + r] = shared[cg] ? mout_of_entry[q] : 0u;
       }
       for (int j = rlen(i); j < W; j++) col[j * R + r] = (unsigned)np_max;  // ELL padding: zero slot, value +0
+      if (bnd) ((double*)(blk + L.o_n2))[r] = nrm2[i];  // ||a~_i||^2 (row_sqnorms: the oracle's O1 order)
       len[r] = (unsigned short)rlen(i);
       fv[r] = 0.0;  // f~ is scattered in per solve (k2_scatter_f)
       orig_q.push_back(p.perm[i]);
@@ -1556,8 +1931,8 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   // CTA size: each compute warp takes about one slice per task with 7 warps when tasks are small
   // (register-resident boundary slices, 256 threads); tasks of many slices (config 5: ~16) need
   // the 15 compute warps of the 512-thread instantiation (measured: 84.6 vs 70.5 us/sweep)
-  k->nt = (double)smeta.size() / std::max<size_t>(tmeta.size(), 1) > 10.0 ? 512 : 256;
-  if (const char* e = getenv("POBK_K2_THREADS")) k->nt = atoi(e) == 512 ? 512 : 256;  // development override
+  k->nt = nt_choice;
+  k->vl = vl_plan;
   k->nsl_max = nsl_max;
   k->nck_max = nck_max;
   k->ntask_max = ntask_max;
@@ -1617,6 +1992,33 @@ bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why) {
   return true;
 }
 
+namespace {
+// the sweep kernel for a plan shape: threads per CTA, vector-slice width, interior mode
+const void* k2_kernel(int nt, int vl, bool ireg) {
+  if (nt == 512) return vl ? (const void*)k2_sweeps<512, false, 8, false> : (const void*)k2_sweeps<512, false, 0, false>;
+  switch (vl) {
+    case 4: return ireg ? (const void*)k2_sweeps<256, true, 4, true> : (const void*)k2_sweeps<256, true, 4, false>;
+    case 8: return ireg ? (const void*)k2_sweeps<256, true, 8, true> : (const void*)k2_sweeps<256, true, 8, false>;
+    default: return ireg ? (const void*)k2_sweeps<256, true, 0, true> : (const void*)k2_sweeps<256, true, 0, false>;
+  }
+}
+// The dynamic shared-memory limit of a sweep kernel is raised once per (kernel, device) to the
+// whole budget and never lowered (changing it while another lane's grid of the kernel runs can
+// serialise the lanes; a per-process flag would miss a second device).
+cudaError_t k2_raise_smem(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
+}
+}  // namespace
+
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches) {
   K2Plan& k = *p.k2;
   cudaError_t e;
@@ -1664,6 +2066,9 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.np_max = k.np_max;
   a.trace = nullptr;
   a.trace_sweep = -1;
+  a.nap = getenv("POBK_K2_NAP") ? atoi(getenv("POBK_K2_NAP")) : 0;  // (development knobs)
+  a.strict = getenv("POBK_K2_STRICT") ? atoi(getenv("POBK_K2_STRICT")) : 0;
+  a.ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 1;
   static const char* trace_env = getenv("POBK_K2_TRACE");
   if (trace_env) {
     const size_t n = (size_t)k.T * k.ntask_max * 12;
@@ -1673,16 +2078,10 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const void* fn = k.nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<POBK_K2_NTB, POBK_K2_BREGB != 0>;
-  // the attribute is raised once to the whole budget (never changed between launches: changing a
-  // function's attribute while another lane's grid of it runs can serialise the lanes)
-  static int attr_set[2] = {0, 0};
-  int& done = attr_set[k.nt == 512 ? 1 : 0];
-  if (!done) {
-    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal)) != cudaSuccess) return e;
-    done = 1;
-  }
-  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt == 512 ? 512 : POBK_K2_NTB), args, k.smem, s);
+  const int ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 0;  // (development knob)
+  const void* fn = k2_kernel(k.nt, k.vl, ireg != 0);
+  if ((e = k2_raise_smem(fn)) != cudaSuccess) return e;
+  e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py
     const size_t n = (size_t)k.T * k.ntask_max * 12;

@@ -103,7 +103,7 @@ cudaError_t k4_solve(Plan& p, cudaStream_t s, long long& launches);
 void k4_free(Plan& p);
 int k4_cluster_size(const Plan& p);
 // cuda/k2_wavefront.cu
-bool k2_build(Plan& p, const HostCSR& At, int tile_rows, std::string& why);
+bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why);
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
 struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; };
 bool k2_stats(const Plan& p, K2Stats& st);

@@ -38,3 +38,22 @@ print("last - first arrival (cycles) p10/p50/p90:", q(spread))
 print("  ... when the last is a look-ahead warp:", q(spread[last_la]), " else:", q(spread[~last_la]))
 per = np.diff(np.where(ok, rel, 0), axis=1)
 print("barrier-to-barrier (cycles) p10/p50/p90:", q(per[(per > 0) & (per < 1e6)]))
+# per-warp detail for one tile: arrival at the barrier closing task ti, relative to the release of
+# barrier ti-1, with the warp's slices in task ti (b = boundary, i = interior; rot as the kernel)
+o = 16 + T * ntm * 96
+tm = np.frombuffer(raw[o:o + ntt * 16], np.int32).reshape(ntt, 4); o += ntt * 16
+tt = np.frombuffer(raw[o:o + (T + 1) * 4], np.int32)
+t = int(sys.argv[3]) if len(sys.argv) > 3 else T // 2
+nw = 7; rot = 0
+print("tile", t)
+for ti in range(tt[t + 1] - tt[t]):
+    nb = tm[tt[t] + ti][1] & 0xffff; ni = tm[tt[t] + ti][1] >> 16; ntot = nb + ni
+    own = {w: "" for w in range(nw)}
+    for q in range(ntot):
+        own[(q + rot) % nw] += "b" if q < nb else "i"
+    rot = (rot + ntot % nw) % nw
+    if ti == 0 or not ok[t, ti]:
+        continue
+    base = rel[t, ti - 1]
+    cells = " ".join(f"w{w}:{own[w] or '-':>3s}{'*' if (lam[t, ti] >> w) & 1 else ' '}{arr[t, ti, w] - base:6d}" for w in range(nw))
+    print(f"task {ti:2d} nb {nb} ni {ni} | {cells} | release {rel[t, ti] - base}")
