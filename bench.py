@@ -16,8 +16,10 @@ config at row granularity; the protocol fixes 1e-1 for configs 3-5).
   roofline   = the sweep kernel: algorithmic bytes B = 12 nnz + 12 m per sweep
                x sweeps / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline = the oracle (plain C, 1 core) on a bounded sample of the same workload
-Multi-GPU: every rank solves its own independent system (distinct x* seed): weak scaling, no
-data-path collective; NCCL only for the barrier and the max-over-ranks time.
+Multi-GPU: every rank solves its own independent systems (config 4: the same matrix with the rank's
+own x*; --config batch9pt_1024: the batched config 5, systems rank*8 .. rank*8+7, 8 per GPU): weak
+scaling, no data-path collective; NCCL only for the barrier, the max-over-ranks time and the
+all_gather of per-system reports (C1) printed under "systems".
 """
 from __future__ import annotations
 
@@ -203,10 +205,13 @@ def main():
     dev = torch.device("cuda", local)
     tol = TOL[a.config]
 
-    # ---- inputs (synthetic, BASELINE.json configs) and preprocessing: once, untimed
-    systems = [gen.make(a.config, rank)]
+    # ---- inputs (synthetic, BASELINE.json configs) and preprocessing: once, untimed.  Every rank
+    #      solves its own systems: config 5 ids rank*8 .. rank*8+7; single-system configs system
+    #      `rank` (the same matrix, its own x*: gen.CONFIGS)
+    ids = [rank]
     if a.config == "batch9pt_1024":
-        systems = [gen.make(a.config, rank * 8 + b) for b in range(8)]   # 8 independent systems per GPU
+        ids = [rank * 8 + b for b in range(8)]   # 8 independent systems per GPU
+    systems = [gen.make(a.config, i) for i in ids]
     # batched systems: half-GPU tilings, so pobk_solve_batch runs two systems side by side
     tile_rows = pk.half_gpu_tile_rows(systems[0].m, local) if a.config == "batch9pt_1024" and a.kernel == "auto" else 0
     plans = [pk.Plan.from_system(s, kernel=a.kernel, device=local, tile_rows=tile_rows) for s in systems]
@@ -285,8 +290,11 @@ def main():
     e2e_updates = float(sum(r.sweeps * p.nnz for r, p in zip(e2e_reps, plans * a.steps)))
     err = max(float(np.linalg.norm(x.cpu().numpy() - s.x_star) / np.linalg.norm(s.x_star)) for x, s in zip(xs, systems))
 
+    from paper_2401_00672_b200 import driver
+    # C1: per-system reports of the last timed step gathered from every rank (all_gather)
+    agg = driver.gather_reports([driver.system_report(i, p.nnz, r) for i, p, r in zip(ids, plans, all_reps[-len(plans):])],
+                                t, dev)
     if world > 1:
-        from paper_2401_00672_b200 import driver
         t, t_e2e, sweep_t = (driver.max_over_ranks(v, dev) for v in (t, t_e2e, sweep_t))
         updates, e2e_updates = (driver.sum_over_ranks(v, dev) for v in (updates, e2e_updates))
     if rank != 0:
@@ -304,6 +312,17 @@ def main():
     # step; the sweep kernels are ~98% of it, profiles/*_launches.md)
     lanes = len(plans) > 1 and sweep_t > 1.05 * t
     kern_t = t if lanes else sweep_t
+    # lanes pobk_solve_batch used (its rule: every plan K2, min(4, SMs / max tiles, systems))
+    nlanes = None
+    if len(plans) > 1:
+        st_all = [p.layout_stats() for p in plans]
+        if all(x["kernel"] == "wavefront" for x in st_all):
+            sms = torch.cuda.get_device_properties(local).multi_processor_count
+            nlanes = max(1, min(4, sms // max(x["ntiles"] for x in st_all), len(plans)))
+        else:
+            nlanes = 1
+    l2_bytes = 126e6
+    resident = B * len(systems) <= l2_bytes
     achieved = B * sweeps / kern_t / 1e9 if kern_t > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -331,18 +350,22 @@ def main():
         "config": {"workload": s0.name if a.config != "batch9pt_1024" else f"{a.config} x8 per GPU",
                    "m": s0.m, "nnz": s0.nnz, "systems_per_gpu": len(systems), "tol_rse": tol, "stop": "rse",
                    "sweeps_per_solve": all_reps[0].sweeps, "kernel": all_reps[0].as_dict()["kernel"],
-                   "batch_lanes": (2 if lanes else 1) if len(plans) > 1 else None,
+                   "batch_lanes": nlanes,
                    "tiles": stats["ntiles"], "private_nnz_frac": round(stats["private_nnz_frac"], 4),
                    "nsteps": plans[0].nsteps, "bandwidth_rcm": plans[0].bw_after,
                    "preprocess_s": round(plans[0].preprocess_seconds, 3),
-                   "l2": "inputs larger than L2 (A stream %.0f MB > 126 MB), no flush" % (B / 1e6),
+                   "l2": ("working set %.1f MB fits the 126 MB L2: L2-resident by design (no flush); the HBM "
+                          "fraction below is not a bound for it" % (B * len(systems) / 1e6)) if resident else
+                         ("inputs larger than L2 (A stream %.0f MB per GPU > 126 MB), no flush" % (B * len(systems) / 1e6)),
                    "time_to_tol_ms": sum(r.solve_seconds for r in all_reps) / len(all_reps) * 1e3,
                    "final_rse": all_reps[-1].final_value, "rel_err_vs_xstar": err},
         "e2e": {"value": e2e_updates / t_e2e, "unit": "nnz-updates/s",
                 "h2d_bytes_per_step": int(sum(3 * 8 * s.m for s in systems)),
                 "d2h_bytes_per_step": int(sum(8 * s.m for s in systems))},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "systems": [{"rank": pr["rank"], "ids": [r["id"] for r in pr["systems"]], "sweeps": [r["sweeps"] for r in pr["systems"]],
+                     "final_rse": [r["final"] for r in pr["systems"]]} for pr in agg["ranks"]],
+        "roofline": {"bound": "l2" if resident else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "sweep (" + all_reps[0].as_dict()["kernel"] + ")", "peak_source": peak_src,
                      "bytes_per_sweep": B, "us_per_sweep": kern_t / sweeps * 1e6,

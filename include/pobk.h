@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define POBK_ABI_VERSION 1
+#define POBK_ABI_VERSION 2
 
 typedef struct pobk_plan_s* pobk_plan_t;
 typedef int32_t pobk_status;
@@ -88,19 +88,27 @@ typedef struct {
 
 typedef struct {
   double tol;           /* default 1e-6; stop when value < tol (strict) */
-  int64_t max_sweeps;   /* default 500000 */
+  int64_t max_sweeps;   /* default 500000: cap on the TOTAL sweep count, sweep_offset
+                           included (the paper's "number of iterations exceeds 5e+5") */
   int32_t stop;         /* POBK_STOP_*; default POBK_STOP_RSE */
   int32_t check_every;  /* check after every k-th sweep; default 1 (needed for +-1 parity) */
+  int64_t sweep_offset; /* resume: sweeps already applied to x0 by earlier calls (default 0).  The
+                           sweeps of this call are numbered from sweep_offset + 1, so checks fall
+                           on the same sweep numbers (multiples of check_every) and the cap on the
+                           same total as in one uninterrupted solve; >= 0 */
 } pobk_solve_opts;
 
 typedef struct {
   int64_t sweeps;        /* sweeps performed by this call */
-  int32_t termination;   /* POBK_TERM_* */
+  int32_t termination;   /* POBK_TERM_* (MAX_SWEEPS: the paper's "Inf"/"NAN" record) */
   int32_t kernel;        /* POBK_KERNEL_* actually used */
   double final_value;    /* last checked RSE or RELRES (NaN with POBK_STOP_NONE) */
   double solve_seconds;  /* CUDA-event time of the whole solve on `stream` (permute in .. out) */
   double sweep_seconds;  /* CUDA-event time of the sweep kernel(s) alone */
   int64_t launches;      /* kernels launched by this call (graph-launched nodes included) */
+  int64_t sweeps_total;  /* sweep_offset + sweeps (the paper's iteration count IT) */
+  double final_rse;      /* last checked RSE; NaN unless stop = POBK_STOP_RSE */
+  double final_relres;   /* last checked ||f - A x|| / ||f||; NaN unless stop = POBK_STOP_RELRES */
 } pobk_report;
 
 void pobk_preprocess_opts_default(pobk_preprocess_opts* o);
@@ -116,7 +124,9 @@ pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* co
                             const pobk_preprocess_opts* opts, int device, pobk_plan_t* out);
 
 /* Sizes and preprocessing statistics; any output pointer may be NULL.  nsteps = number of
- * schedule steps (Oclass categories + Nclass rows); bandwidths are max |i - j| before/after. */
+ * schedule steps = ncat, the number of first-fit categories: every category is one step -- the
+ * Oclass categories (>= 2 rows, n_oclass of them) and the Nclass rows (singleton categories,
+ * P:220); bandwidths are max |i - j| before/after RCM (Table 1). */
 pobk_status pobk_plan_info(pobk_plan_t plan, int64_t* m, int64_t* nnz, int32_t* nsteps, int32_t* n_oclass,
                            int64_t* bw_before, int64_t* bw_after, double* preprocess_seconds);
 
@@ -155,7 +165,9 @@ pobk_status pobk_solve(pobk_plan_t plan, const double* f_dev, double* x_dev, con
 pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const double* xstar,
                             const pobk_solve_opts* opts, void* stream, pobk_report* rep);
 
-/* nb independent systems (one plan each, same device); every system stops on its own rule.
+/* Alg 5 for nb independent systems (one plan each, same device; the batched
+ * configuration of the north star, one shard of a multi-GPU batch): every system stops on its
+ * own rule.  All arguments are checked before anything is enqueued.
  * Arrays of nb device pointers; reps[nb].  Ordered after prior work on `stream`, and `stream`
  * waits for all of them.  When every plan is a K2 (wavefront) plan and L >= 2 of their grids fit
  * the device side by side (plans built with tile_rows covering at most 1/L of the SMs), system b
@@ -166,12 +178,14 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
                              pobk_report* reps);
 
 /* *out = ||f - A x||_2 in the user frame (fused SpMV + squared-norm kernel, deterministic
- * two-level reduction).  Device vectors; result returned to the host. */
+ * two-level reduction): the residual of Ax = f whose ratio to ||f|| is the RELRES stop
+ * (SURVEY Z13), the paper's RSE needing x*.  Device vectors; result returned to the host. */
 pobk_status pobk_residual_norm(pobk_plan_t plan, const double* f_dev, const double* x_dev, void* stream,
                                double* out);
 
 /* *out = sum_{row_begin <= i < row_end} (f_i - a_i . x)^2 over USER-frame rows (the per-rank part
- * of a row-sharded residual; combine across ranks with an all-reduce SUM). */
+ * of a row-sharded residual for the convergence check; combine across ranks with an
+ * all-reduce SUM, then sqrt). */
 pobk_status pobk_residual_sumsq_rows(pobk_plan_t plan, int64_t row_begin, int64_t row_end, const double* f_dev,
                                      const double* x_dev, void* stream, double* out);
 

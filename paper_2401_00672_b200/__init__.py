@@ -39,13 +39,14 @@ def _stream(stream):
     return ctypes.c_void_p(int(stream))
 
 
-def _solve_opts(tol, max_sweeps, stop, check_every) -> L.SolveOpts:
+def _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset=0) -> L.SolveOpts:
     o = L.SolveOpts()
     L.lib.pobk_solve_opts_default(ctypes.byref(o))
     o.tol = float(tol)
     o.max_sweeps = int(max_sweeps)
     o.stop = L.STOP[stop] if isinstance(stop, str) else int(stop)
     o.check_every = int(check_every)
+    o.sweep_offset = int(sweep_offset)
     return o
 
 
@@ -110,23 +111,24 @@ class Plan:
 
     # ------------------------------------------------------------ solves
     def solve(self, f, x, x_star=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse", check_every: int = 1,
-              stream=None) -> Report:
-        """x (CUDA float64, user frame) is x0 on entry and the solution on exit."""
+              stream=None, sweep_offset: int = 0) -> Report:
+        """x (CUDA float64, user frame) is x0 on entry and the solution on exit; sweep_offset > 0
+        resumes a solve whose x0 already had that many sweeps (same check numbering and total cap)."""
         rep = L.Report()
-        o = _solve_opts(tol, max_sweeps, stop, check_every)
+        o = _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset)
         L.check(L.lib.pobk_solve(self._h, _dev_ptr(f, "f", self.m), _dev_ptr(x, "x", self.m),
                                  _dev_ptr(x_star, "x_star", self.m), ctypes.byref(o), _stream(stream), ctypes.byref(rep)))
         return rep
 
     def solve_host(self, f: np.ndarray, x: np.ndarray, x_star=None, tol: float = 1e-6, max_sweeps: int = 500000,
-                   stop="rse", check_every: int = 1, stream=None) -> Report:
+                   stop="rse", check_every: int = 1, stream=None, sweep_offset: int = 0) -> Report:
         """End-to-end path with host arrays (x is updated in place)."""
         for name, a in (("f", f), ("x", x), ("x_star", x_star)):
             if a is not None and (not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous
                                   or a.size != self.m):
                 raise TypeError(f"{name} must be a contiguous float64 numpy array of length {self.m}")
         rep = L.Report()
-        o = _solve_opts(tol, max_sweeps, stop, check_every)
+        o = _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset)
         L.check(L.lib.pobk_solve_host(self._h, L.ptr(f), L.ptr(x), L.ptr(x_star) if x_star is not None else None,
                                       ctypes.byref(o), _stream(stream), ctypes.byref(rep)))
         return rep

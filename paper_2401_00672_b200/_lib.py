@@ -29,7 +29,7 @@ class PreprocessOpts(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_sweeps", ctypes.c_int64), ("stop", ctypes.c_int32),
-                ("check_every", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("sweep_offset", ctypes.c_int64)]
 
 
 class LayoutStats(ctypes.Structure):
@@ -46,13 +46,15 @@ class LayoutStats(ctypes.Structure):
 class Report(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int64), ("termination", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("final_value", ctypes.c_double), ("solve_seconds", ctypes.c_double),
-                ("sweep_seconds", ctypes.c_double), ("launches", ctypes.c_int64)]
+                ("sweep_seconds", ctypes.c_double), ("launches", ctypes.c_int64), ("sweeps_total", ctypes.c_int64),
+                ("final_rse", ctypes.c_double), ("final_relres", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {"sweeps": int(self.sweeps), "termination": TERM_NAME.get(self.termination, self.termination),
                 "kernel": KERNEL_NAME.get(self.kernel, self.kernel), "final_value": float(self.final_value),
                 "solve_seconds": float(self.solve_seconds), "sweep_seconds": float(self.sweep_seconds),
-                "launches": int(self.launches)}
+                "launches": int(self.launches), "sweeps_total": int(self.sweeps_total),
+                "final_rse": float(self.final_rse), "final_relres": float(self.final_relres)}
 
 
 class PobkError(RuntimeError):

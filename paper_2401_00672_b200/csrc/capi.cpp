@@ -10,6 +10,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "plan.h"
 
@@ -153,11 +154,11 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
   CUDA_TRY(launch_permute_in(p, f, x, xstar, p.d_fs, p.d_xt, o.stop == POBK_STOP_RSE ? p.d_xst : nullptr, s, launches));
   CUDA_TRY(launch_init_ctrl(p, o, s, launches));
   CUDA_TRY(cudaEventRecord(p.ev[1], s));
-  // K2 evaluates RSE and fixed counts in-kernel; a RELRES stop runs on the K1 graph loop (its
-  // check kernel carries the fused residual SpMV + norm).
+  // K2 evaluates RSE, RELRES (a residual pass over each tile's stream) and fixed counts in-kernel;
+  // plans with vector boundary slices (opt-in) take RELRES on the K1 graph loop.
   int used = p.kernel;
-  if (used == POBK_KERNEL_WAVEFRONT && o.stop == POBK_STOP_RELRES) used = POBK_KERNEL_LAUNCH;
-  if (o.max_sweeps > 0) {
+  if (used == POBK_KERNEL_WAVEFRONT && o.stop == POBK_STOP_RELRES && !k2_relres_ok(p)) used = POBK_KERNEL_LAUNCH;
+  if (o.max_sweeps - o.sweep_offset > 0) {
     switch (used) {
       case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
       case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, f, s, launches)); break;
@@ -184,12 +185,16 @@ pobk_status solve_finish(Plan& p, const pobk_solve_opts& o, pobk_report* rep) {
   CUDA_TRY(cudaEventElapsedTime(&t_all, p.ev[0], p.ev[3]));
   CUDA_TRY(cudaEventElapsedTime(&t_sw, p.ev[1], p.ev[2]));
   const Ctrl& c = *p.h_ctrl;
-  if (used == POBK_KERNEL_LAUNCH && o.max_sweeps > 0) launches += c.sweeps * p.k1_nodes_per_sweep;
+  const bool ran = o.max_sweeps - o.sweep_offset > 0;
+  if (used == POBK_KERNEL_LAUNCH && ran) launches += c.sweeps * p.k1_nodes_per_sweep;
   if (rep) {
-    rep->sweeps = o.max_sweeps > 0 ? c.sweeps : 0;
+    rep->sweeps = ran ? c.sweeps : 0;
     rep->termination = c.term;
     rep->kernel = used;
     rep->final_value = (o.stop == POBK_STOP_NONE) ? NAN : c.value;
+    rep->sweeps_total = o.sweep_offset + rep->sweeps;
+    rep->final_rse = o.stop == POBK_STOP_RSE ? rep->final_value : NAN;
+    rep->final_relres = o.stop == POBK_STOP_RELRES ? rep->final_value : NAN;
     rep->solve_seconds = t_all * 1e-3;
     rep->sweep_seconds = t_sw * 1e-3;
     rep->launches = launches;
@@ -208,6 +213,7 @@ pobk_status check_solve_args(pobk_plan_t plan, const void* f, const void* x, con
   if (o.stop == POBK_STOP_RSE && !xstar) return fail(POBK_ERR_ARG, "POBK_STOP_RSE needs xstar");
   if (o.check_every < 1) return fail(POBK_ERR_ARG, "opts.check_every must be >= 1");
   if (o.max_sweeps < 0) return fail(POBK_ERR_ARG, "opts.max_sweeps must be >= 0");
+  if (o.sweep_offset < 0) return fail(POBK_ERR_ARG, "opts.sweep_offset must be >= 0");
   if (!(o.tol >= 0.0)) return fail(POBK_ERR_ARG, "opts.tol must be >= 0");
   return POBK_OK;
 }
@@ -234,6 +240,7 @@ void pobk_solve_opts_default(pobk_solve_opts* o) {
   o->max_sweeps = 500000;
   o->stop = POBK_STOP_RSE;
   o->check_every = 1;
+  o->sweep_offset = 0;
 }
 
 int32_t pobk_abi_version(void) { return POBK_ABI_VERSION; }
@@ -402,6 +409,15 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
   // by side (e.g. plans built with half-GPU tiles), system b runs on internal stream b mod nl, so
   // nl cooperative sweep kernels share the GPU (each system's latency-bound step chain overlaps
   // the others').  Results are those of back-to-back solves (tiling never changes them).
+  // every system's arguments are checked before anything is enqueued
+  std::vector<pobk_solve_opts> os(nb);
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
+    if (st != POBK_OK) {
+      g_err = "system " + std::to_string(b) + ": " + g_err;
+      return st;
+    }
+  }
   bool lanes = nb >= 2;
   int sms = 148, dev = -1;
   for (int32_t b = 0; b < nb && lanes; b++) {
@@ -409,6 +425,11 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
     else if (dev >= 0 && plans[b]->device != dev) lanes = false;
     else dev = plans[b]->device;
   }
+  // a plan is not re-entrant (its vectors, control block and events serve one solve at a time):
+  // a batch that names a plan twice runs back to back, each solve reported before the next
+  for (int32_t b = 0; b < nb && lanes; b++)
+    for (int32_t c = 0; c < b && lanes; c++)
+      if (plans[c] == plans[b]) lanes = false;
   int nl = 1;  // lanes: as many K2 grids as fit side by side (at most 4)
   if (lanes) {
     int v = 0;  // (cudaGetDeviceProperties costs milliseconds; the attribute query does not)
@@ -441,22 +462,24 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaEventRecord(lane_ev[4], s));
   for (int i = 0; i < nl; i++) CUDA_TRY(cudaStreamWaitEvent(lane_s[i], lane_ev[4], 0));
-  std::vector<pobk_solve_opts> os(nb);
-  for (int32_t b = 0; b < nb; b++) {
-    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
-    if (st == POBK_OK)
-      st = solve_device(*plans[b], f[b], x[b], os[b].stop == POBK_STOP_RSE && xstar ? xstar[b] : nullptr, os[b], lane_s[b % nl],
-                        nullptr, true);
-    if (st != POBK_OK) {
-      g_err = "system " + std::to_string(b) + ": " + g_err;
-      return st;
-    }
+  pobk_status enq = POBK_OK;
+  for (int32_t b = 0; b < nb && enq == POBK_OK; b++) {
+    enq = solve_device(*plans[b], f[b], x[b], os[b].stop == POBK_STOP_RSE && xstar ? xstar[b] : nullptr, os[b], lane_s[b % nl],
+                       nullptr, true);
+    if (enq != POBK_OK) g_err = "system " + std::to_string(b) + ": " + g_err;
   }
+  // (also after a failed enqueue: `stream` is ordered after everything already enqueued and the
+  // lanes are drained, so no solve of this call outlives it)
+  const std::string keep = g_err;
   for (int i = 0; i < nl; i++) {
     CUDA_TRY(cudaEventRecord(lane_ev[i], lane_s[i]));
     CUDA_TRY(cudaStreamWaitEvent(s, lane_ev[i], 0));
   }
   for (int i = 0; i < nl; i++) CUDA_TRY(cudaStreamSynchronize(lane_s[i]));
+  if (enq != POBK_OK) {
+    g_err = keep;
+    return enq;
+  }
   for (int32_t b = 0; b < nb; b++) {
     pobk_status st = solve_finish(*plans[b], os[b], reps ? reps + b : nullptr);
     if (st != POBK_OK) return st;

@@ -1,6 +1,7 @@
 // K2: persistent tiled wavefront sweep.
 //
-// The rows of A~ are split into T tiles (one 512-thread CTA per SM, cooperative launch).  A
+// The rows of A~ are split into T tiles, one CTA per SM (cooperative launch; 256 threads = 7
+// compute warps + 1 TMA producer warp, or 512 threads = 15 + 1 when tasks have many slices).  A
 // schedule step (a category of pairwise-orthogonal rows) restricted to one tile is a
 // "task".  The sequential semantics of a sweep (Alg 5 loop) only order rows that
 // share a column.  Columns touched by one tile only are "private" (kept in that CTA's shared
@@ -24,24 +25,31 @@
 //  * Rows are stored as SLICES of <= 32 rows, one lane per row, in ELL order inside the slice
 //    (entry j of lane r at j*R + r; a task's rows are sorted by length before slicing so the
 //    padding is small; padding entries are value +0 on a private "zero slot" column): coalesced,
-//    conflict-free val/col loads, the row sum runs left to right in one thread (the oracle's
-//    order) and ||a~_i||^2 is recomputed in registers from the row (the oracle's left-to-right
-//    sum), so a row streams 12 B per stored entry + 10 B (f~, length), and a boundary row another
-//    4 B per entry (the mailbox slot its new value goes to).
+//    conflict-free val/col loads; the row sum runs left to right in one thread (the oracle's
+//    order).  An interior row recomputes ||a~_i||^2 in registers (the oracle's left-to-right sum)
+//    and streams 12 B per stored entry + 10 B (f~, length); a boundary row also streams its
+//    ||a~_i||^2 (8 B, the host's row_sqnorms in the same order) and 4 B per entry (the mailbox
+//    slot its new value goes to), all loaded before the task barrier.
+//  * Opt-in vector boundary slices (VSlice, POBK_K2_VL=4|8): L lanes per boundary row, row sum
+//    in the oracle's order through the slice's ring slot -- bitwise equal, measured slower on the
+//    BASELINE configs, kept as an option.
 //  * A task's boundary slices come first; their warps note the shared entries, poll the
 //    mailboxes, then read the private operands with the row sums; the interior slices run
 //    meanwhile on the other warps.
 //  * The tile's slices are packed, across task boundaries, into <= 16 KB chunks streamed by 1-D
-//    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (warp 15),
-//    which never touches x~.
-//  * The RSE is evaluated at the end of each sweep by each tile over the columns
-//    it owns (its private ones, x~ in shared memory, and the shared ones whose last writer in the
-//    sweep it holds, read from the wrap mailbox slot), x~* read from per-tile contiguous arrays
-//    gathered once per solve.  Partials are combined in fixed orders; one grid-wide decision per
-//    sweep.
-//  * A task's slices, boundary first, go round-robin over the 15 compute warps, so consecutive
-//    boundary slices (the critical path: their post phases start together when the neighbours'
-//    data arrives) run on different SM sub-partitions.
+//    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (the last
+//    warp), which never touches x~.
+//  * Stop checks at the end of a due sweep.  RSE: each tile sums (x~ - x~*)^2
+//    over the columns it owns (its private ones, x~ in shared memory, and the shared ones whose
+//    last writer in the sweep it holds, read from the wrap mailbox slot), x~* from per-tile
+//    contiguous arrays gathered once per solve.  RELRES: the owners publish the shared columns'
+//    sweep-final values to global x~, a grid barrier, then a residual pass over each tile's own
+//    stream.  Partials are combined in fixed orders; one grid-wide decision per sweep (every
+//    tile forms the same total from the same partials).
+//  * A task's slices, boundary first, go round-robin over the compute warps (the round-robin
+//    continuing across tasks), so consecutive boundary slices run on different SM sub-partitions.
+//  * One kernel instantiation per plan shape (threads, vector-slice width, interior mode): all
+//    paths inlined into one kernel spilled registers and doubled the sweep time.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,7 +57,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
-#include <mutex>
 #include <set>
 #include <string>
 #include <vector>
@@ -97,9 +104,15 @@ struct SliceLayout {
 };
 
 struct SyncState {
-  unsigned int arrive;  // monotonic: T per completed sweep
-  int pad0[31];
+  unsigned long long arrive;   // monotonic: T per completed sweep (64-bit: no wrap at any sweep count)
+  unsigned long long arrive2;  // monotonic: T per RELRES publication (x~ of the shared columns)
+  long long pad0[14];
 };
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 struct K2Args {
   const unsigned char* stream;
@@ -134,14 +147,15 @@ struct K2Args {
 };
 
 // shared-memory control block
-struct Ctl {
+struct alignas(16) Ctl {  // (16-byte multiple: the int4 metadata follows it in shared memory)
   unsigned long long full[kMaxSlots];  // TMA completion mbarriers
   int released[kMaxSlots];             // slices consumed per slot (cumulative)
   unsigned long long issued;           // chunks issued (sequence number)
   int stop;
-  int done;                            // sweeps completed (all tiles stop at the same sweep)
+  long long done;                      // sweeps completed (all tiles stop at the same sweep)
   double part[32];                     // per-compute-warp RSE partials
 };
+static_assert(sizeof(Ctl) % 16 == 0, "int4 metadata follows Ctl in shared memory");
 
 // ------------------------------------------------------------------ PTX helpers (TMA, mbarrier)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -203,9 +217,6 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 __device__ __forceinline__ void named_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-// Development ablations (wrong numerics; timing only): bit 0 no mailbox wait, bit 1 no per-task
-// barrier, bit 2 interior slices skipped, bit 3 boundary post skipped, bit 4 every slice skipped,
-// bit 5 no private stores in the boundary write-back, bit 6 weak mailbox stores, bit 7 no re-arm.
 #ifndef POBK_K2_PSLEEP
 #define POBK_K2_PSLEEP 64  // producer back-off while its next ring slot is still in use (ns)
 #endif
@@ -218,16 +229,6 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 #ifndef POBK_K2_PRIO
 #define POBK_K2_PRIO 1  // boundary priority on the 256-thread path (measured 1-2% faster, configs 3-4)
 #endif
-#ifndef POBK_K2_NTB
-#define POBK_K2_NTB 256  // threads of the register-resident (BSlice2) instantiation
-#endif
-#ifndef POBK_K2_BREGB
-#define POBK_K2_BREGB 1  // development: 0 = that instantiation uses BSlice
-#endif
-#ifndef POBK_K2_ABL
-#define POBK_K2_ABL 0
-#endif
-constexpr int kAbl = POBK_K2_ABL;
 
 // ------------------------------------------------------------------ slice arithmetic
 // All shared-memory operands are addressed through 32-bit shared-window addresses held in
@@ -296,10 +297,6 @@ __device__ __forceinline__ void stm4_if(unsigned p, unsigned long long* a, unsig
                : "memory");
 }
 __device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsigned long long v) {
-  if (POBK_K2_ABL & 64) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a), "l"(v) : "memory");
-    return;
-  }
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.b64 [%1], %2;\n}" ::"r"(p), "l"(a),
                "l"(v)
                : "memory");
@@ -416,14 +413,13 @@ struct BSlice {
       for (int j = 0; j < kMaxJ; j++)
         if ((pend >> j) & 1u) np |= ((unsigned long long)__double_as_longlong(xr[j]) == kSentinel) ? (1u << j) : 0u;
       pend = np;
-      if (kAbl & 1) break;
       if (!__any_sync(kFull, pend != 0u)) break;
     }
     if (trp && (threadIdx.x & 31) == 0) trp[11] = (unsigned long long)it;
     // re-arm the consumed slots for the sweep after next (ordered by the per-sweep grid barrier)
 #pragma unroll
     for (int j4 = 0; j4 < kMaxJ; j4 += 4)
-      if (j4 < W && !(kAbl & 128)) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
+      if (j4 < W) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
   // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
@@ -522,7 +518,7 @@ struct BSlice {
         for (int u = 0; u < kBatch; u++) {
           const int j = jb + u;
           const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
-          if (!(kAbl & 32)) sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
+          sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
           stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
                  (unsigned long long)__double_as_longlong(xr[j]));
         }
@@ -955,6 +951,40 @@ __device__ __forceinline__ void slice_interior_reg(const SliceAddr& S, int W, un
   }
 }
 
+// interior slice, all operands register-resident (the kIReg = 2 instantiation, W <= kMaxJ):
+// columns and values, then the x~ they address -- two dependent shared-memory round trips per
+// slice in total -- and no second read in the update pass.  Same operations in the same order
+// (common.cuh).
+constexpr int kIJ = 20;  // register window of slice_interior_reg2 (config 4: rows of 15-28 entries, p99 22)
+__device__ __forceinline__ void slice_interior_reg2(const SliceAddr& S, int W, unsigned xb) {
+  unsigned c[kIJ];
+  double av[kIJ], xv[kIJ];
+#pragma unroll
+  for (int j = 0; j < kIJ; j++) {
+    const unsigned in = j < W ? 1u : 0u;
+    c[j] = lds32_if(in, S.cb + (unsigned)j * S.cs);
+    av[j] = 0.0;
+    lds64_if(av[j], in, S.vb + (unsigned)j * S.vs);
+  }
+#pragma unroll
+  for (int j = 0; j < kIJ; j++) {
+    xv[j] = 0.0;
+    lds64_if(xv[j], j < W ? 1u : 0u, xb + 8u * c[j]);
+  }
+  double s = 0.0, n2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < kIJ; j++) {
+    if ((j & ~(kBatch - 1)) < W) {  // entries past the width are +0 * +0: bit-exact no-ops
+      s = __dadd_rn(s, __dmul_rn(av[j], xv[j]));
+      n2 = __dadd_rn(n2, __dmul_rn(av[j], av[j]));
+    }
+  }
+  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+#pragma unroll
+  for (int j = 0; j < kIJ; j++)
+    sts64_if(j < S.myl ? 1u : 0u, xb + 8u * c[j], __dadd_rn(xv[j], __dmul_rn(alpha, av[j])));
+}
+
 // one vector boundary slice of lane width L: pre, poll, [barrier], post
 template <int L>
 __device__ __forceinline__ void run_vslice(unsigned blk, int R, int W, int lane, unsigned long long* mbox_s, bool bar,
@@ -973,7 +1003,7 @@ __device__ __forceinline__ void run_vslice(unsigned blk, int R, int W, int lane,
 // kVL: lane width of the plan's vector boundary slices (0: none); kIReg: register-resident
 // interior slices.  One instantiation per plan shape keeps each kernel's register allocation
 // to the paths it runs (every path inlined into one kernel spilled and ran 2x slower).
-template <int kNT, bool kBReg, int kVL, bool kIReg>
+template <int kNT, bool kBReg, int kVL, int kIReg>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
@@ -1023,7 +1053,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       const unsigned char* tbase = a.stream + a.tile_off[t];
       int cum[kMaxSlots];
       for (int i = 0; i < kMaxSlots; i++) cum[i] = 0;
-      const unsigned long long gmax = (unsigned long long)maxs * (unsigned long long)nck;
+      // (RELRES: every checked sweep streams the tile's chunks once more for the residual)
+      const unsigned long long gmax = (mode == POBK_STOP_RELRES ? 2ull : 1ull) * (unsigned long long)maxs * (unsigned long long)nck;
       unsigned long long g = 0;
       int slot = 0, c = 0;
       while (!ld_vol_shared(&ctl->stop)) {
@@ -1050,8 +1081,10 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const unsigned xb = opaque(smem_u32(xloc));
     const unsigned ring_s = opaque(smem_u32(ring));
     long long sweep = 0;
+    long long pass = 0;  // passes over the tile's stream: sweeps + RELRES residual passes
+    long long nres = 0;  // RELRES residual passes done
     const int nck2 = nck % (2 * NS);
-    int hbase = 0;  // (sweep * nck) mod 2NS
+    int hbase = 0;  // (pass * nck) mod 2NS
     while (sweep < maxs) {
       const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
@@ -1095,7 +1128,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           wtp[warp] = clock64();
           if (la) atomicOr(&wtp[7], 1ull << warp);
         }
-        if (!la && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);  // the tile's task ti-1 is complete
+        if (!la && ti > 0) named_bar(1, kNC);  // the tile's task ti-1 is complete
         if (POBK_K2_WT && wtp && lane == 0 && warp == 0 && !la) wtp[8] = clock64();
 #if POBK_K2_PRIO
         // boundary priority: the interior warps start the task once the look-ahead warps hold
@@ -1114,7 +1147,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           }
           const int4 sl = smeta[tm.x + q];
           const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z & 0xffff, VL = sl.z >> 16;
-          const unsigned long long g = (unsigned long long)sweep * nck + chunk;
+          const unsigned long long g = (unsigned long long)pass * nck + chunk;
           // ring position of chunk g without 64-bit division: h = g mod 2NS from the sweep's base
           // and the chunk's residue (precomputed); slot = h mod NS, phase parity = h >= NS
           int h = hbase + (sl.y >> 16);
@@ -1127,7 +1160,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
           if (kVL > 0 && bnd && VL) {  // vector boundary slice (L lanes per row)
             unsigned long long* const mbox_s = mbox_p + sl.w;
-            const bool bar = la && q == qs && ti > 0 && !(kAbl & 2);
+            const bool bar = la && q == qs && ti > 0;
             const int prio = (kBReg && la && q == qs && !a.strict) ? kNC : 0;
             unsigned long long* const vtr = (tr && q == 0) ? trp : nullptr;
             if constexpr (kVL > 0) run_vslice<kVL>(blk, R, W, lane, mbox_s, bar, kNC, xb, a.mbox, off_p, off_q, vtr, prio, a.nap);
@@ -1141,11 +1174,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             continue;
           }
           const SliceAddr S(blk, R, W, bnd, lane);
-          if (kAbl & 16) {
-            if (la && q == qs && ti > 0 && !(kAbl & 2)) named_bar(1, kNC);
-          } else if (bnd) {
+          if (bnd) {
             unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
-            const bool bar = la && q == qs && ti > 0 && !(kAbl & 2);  // look-ahead slice: barrier after the poll
+            const bool bar = la && q == qs && ti > 0;  // look-ahead slice: barrier after the poll
             if constexpr (kBReg) {
               BSlice2 B;
               B.pre(S, W, R, lane, blk, xb);
@@ -1156,7 +1187,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (bar) named_bar(1, kNC);
               if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs && !a.strict) ? kNC : 0);
+              B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs && !a.strict) ? kNC : 0);
             } else {
               BSlice B;
               B.pre(S, W, xb);
@@ -1167,14 +1198,15 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (bar) named_bar(1, kNC);
               if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-              if (!(kAbl & 8)) B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
+              B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, R, (tr && q == 0) ? trp : nullptr);
             }
             if (tr && q == 0) {
               __syncwarp();
               if (lane == 0) trp[10] = gtimer();
             }
-          } else if (!(kAbl & 4)) {
-            if (kIReg && W <= kMaxJ) slice_interior_reg(S, W, xb);
+          } else {
+            if (kIReg == 2 && W <= kIJ) slice_interior_reg2(S, W, xb);
+            else if (kIReg == 1 && W <= kMaxJ) slice_interior_reg(S, W, xb);
             else slice_interior(S, W, xb);
           }
           __syncwarp();
@@ -1185,12 +1217,75 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       }
       named_bar(1, kNC);  // the sweep's last task is complete
       sweep++;
+      pass++;
       hbase += nck2;
       hbase = hbase >= 2 * NS ? hbase - 2 * NS : hbase;
       // ---- end of sweep: a grid barrier every sweep (it also orders the mailbox re-arms of this
       //      sweep before the writes of the next ones); the stop test when due
-      const bool due = mode == POBK_STOP_RSE && ((sweep % every) == 0 || sweep >= maxs);
-      if (due) {
+      const bool due_check = ((sweep + a.ctrl->offset) % every) == 0 || sweep >= maxs;
+      const bool due = mode != POBK_STOP_NONE && due_check;
+      if (mode == POBK_STOP_RELRES && due_check) {
+        // RELRES = ||f~ - A~ x~||_2 / ||f~||_2 at the end of the sweep (the fused
+        // SpMV + norm of the north star): (1) the last-writer tile of every shared column
+        // publishes the column's sweep-final value (its wrap slot) to x~ in global memory; (2) a
+        // grid barrier; (3) a residual pass over the tile's own stream (the producer streams the
+        // tile's chunks once more), private x~ from shared memory, shared x~ from global memory;
+        // per-row residuals in fixed order per lane, then the fixed-order reductions below.
+        const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB;
+        for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNC)
+          a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + a.lastslot[j], 0ull));
+        __threadfence();
+        named_bar(1, kNC);
+        nres++;
+        if (tid == 0) {
+          atomicAdd(&a.sync->arrive2, 1ull);
+          const unsigned long long target = (unsigned long long)nres * (unsigned long long)a.T;
+          while (ld_acquire_u64(&a.sync->arrive2) < target) {
+          }
+          __threadfence();
+        }
+        named_bar(1, kNC);
+        double acc = 0.0;
+        int rr = 0;  // running slice index: slice rr goes to compute warp rr mod kNCW
+        for (int ti = 0; ti < ntask; ti++) {
+          const int4 tm = tmeta[ti];
+          const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
+          for (int q = 0; q < ntot; q++, rr = rr + 1 == kNCW ? 0 : rr + 1) {
+            if (rr != warp) continue;
+            const int4 sl = smeta[tm.x + q];
+            const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z & 0xffff;
+            const unsigned long long g = (unsigned long long)pass * nck + chunk;
+            int h = hbase + (sl.y >> 16);
+            h = h >= 2 * NS ? h - 2 * NS : h;
+            const int slot = h >= NS ? h - NS : h;
+            while (ld_vol_shared64(&ctl->issued) <= g)
+              if (POBK_K2_CSLEEP) __nanosleep(POBK_K2_CSLEEP);
+            mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
+            const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
+            const SliceAddr S(blk, R, W, q < nbnd, lane);  // (one-lane layout: K2 keeps RELRES off VSlice plans)
+            if (lane < R) {
+              double sr = 0.0;
+              for (int j = 0; j < W; j++) {
+                const unsigned c = lds32(S.cb + j * S.cs);
+                const double av = lds64(S.vb + j * S.vs);
+                const double xv = (c & kShared) ? ld_cg(a.xg + (c & kIdx)) : lds64(xb + 8u * c);
+                sr = __dadd_rn(sr, __dmul_rn(av, xv));
+              }
+              const double r = __dsub_rn(S.f, sr);
+              acc = fma(r, r, acc);
+            }
+            __syncwarp();
+            if (lane == 0) atomicAdd(&ctl->released[slot], 1);
+          }
+        }
+        pass++;
+        hbase += nck2;
+        hbase = hbase >= 2 * NS ? hbase - 2 * NS : hbase;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // fixed lane order
+        if (lane == 0) ctl->part[warp] = acc;
+      }
+      if (mode == POBK_STOP_RSE && due) {
         // columns final for this sweep once the tile's last task is done: the private ones, and
         // the shared ones whose last writer (row of the highest step) is in this tile.  x~* of the
         // private columns is contiguous per tile (16-B loads, prefetched into L2 during the
@@ -1251,13 +1346,13 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             for (int w2 = 0; w2 < kNCW; w2++) part += ((volatile double*)ctl->part)[w2];
           a.partials[par * a.T + t] = part;
           __threadfence();
-          atomicAdd(&a.sync->arrive, 1u);
-          const unsigned target = (unsigned)sweep * (unsigned)a.T;
-          while ((unsigned)ld_acquire((const int*)&a.sync->arrive) < target) {
+          atomicAdd(&a.sync->arrive, 1ull);
+          const unsigned long long target = (unsigned long long)sweep * (unsigned long long)a.T;
+          while (ld_acquire_u64(&a.sync->arrive) < target) {
           }
         }
         __syncwarp();
-        (void)ld_acquire((const int*)&a.sync->arrive);  // (each lane: acquire before reading partials)
+        (void)ld_acquire_u64(&a.sync->arrive);  // (each lane: acquire before reading partials)
         int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
         double v = 0.0;
         if (due) {
@@ -1281,7 +1376,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       }
       named_bar(2, kNC);
       if (ld_vol_shared(&ctl->stop)) {
-        if (tid == 0) ctl->done = (int)sweep;
+        if (tid == 0) ctl->done = sweep;
         break;
       }
     }
@@ -1313,7 +1408,10 @@ __global__ void k2_gather_xs(int n, const int* __restrict__ pmap, int nl, const 
   }
 }
 
-__global__ void k2_reset(SyncState* sync) { sync->arrive = 0; }
+__global__ void k2_reset(SyncState* sync) {
+  sync->arrive = 0;
+  sync->arrive2 = 0;
+}
 
 // every mailbox slot empty, then each shared column's first reader of sweep 0 gets x~0
 __global__ void k2_mbox_fill(unsigned long long* mbox, long long n) {
@@ -1994,28 +2092,15 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
 
 namespace {
 // the sweep kernel for a plan shape: threads per CTA, vector-slice width, interior mode
-const void* k2_kernel(int nt, int vl, bool ireg) {
-  if (nt == 512) return vl ? (const void*)k2_sweeps<512, false, 8, false> : (const void*)k2_sweeps<512, false, 0, false>;
+const void* k2_kernel(int nt, int vl, int ireg) {
+  if (nt == 512) return vl ? (const void*)k2_sweeps<512, false, 8, 0> : (const void*)k2_sweeps<512, false, 0, 0>;
   switch (vl) {
-    case 4: return ireg ? (const void*)k2_sweeps<256, true, 4, true> : (const void*)k2_sweeps<256, true, 4, false>;
-    case 8: return ireg ? (const void*)k2_sweeps<256, true, 8, true> : (const void*)k2_sweeps<256, true, 8, false>;
-    default: return ireg ? (const void*)k2_sweeps<256, true, 0, true> : (const void*)k2_sweeps<256, true, 0, false>;
+    case 4: return (const void*)k2_sweeps<256, true, 4, 0>;
+    case 8: return (const void*)k2_sweeps<256, true, 8, 0>;
+    default:
+      return ireg == 2 ? (const void*)k2_sweeps<256, true, 0, 2>
+                       : ireg == 1 ? (const void*)k2_sweeps<256, true, 0, 1> : (const void*)k2_sweeps<256, true, 0, 0>;
   }
-}
-// The dynamic shared-memory limit of a sweep kernel is raised once per (kernel, device) to the
-// whole budget and never lowered (changing it while another lane's grid of the kernel runs can
-// serialise the lanes; a per-process flag would miss a second device).
-cudaError_t k2_raise_smem(const void* fn) {
-  static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> g(mu);
-  if (done.count({fn, dev})) return cudaSuccess;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal);
-  if (e == cudaSuccess) done.insert({fn, dev});
-  return e;
 }
 }  // namespace
 
@@ -2079,8 +2164,8 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   }
   void* args[] = {&a};
   const int ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 0;  // (development knob)
-  const void* fn = k2_kernel(k.nt, k.vl, ireg != 0);
-  if ((e = k2_raise_smem(fn)) != cudaSuccess) return e;
+  const void* fn = k2_kernel(k.nt, k.vl, ireg);
+  if ((e = raise_smem_limit(fn)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
   if (e == cudaSuccess && a.trace) {  // development aid: raw stamps + the task table for tools/k2_trace.py
@@ -2113,6 +2198,9 @@ void k2_free(Plan& p) {
   delete p.k2;
   p.k2 = nullptr;
 }
+
+// RELRES runs inside K2 on one-lane layouts (the residual pass reads slices in that layout)
+bool k2_relres_ok(const Plan& p) { return p.k2 && p.k2->vl == 0; }
 
 bool k2_stats(const Plan& p, K2Stats& st) {
   if (!p.k2) return false;

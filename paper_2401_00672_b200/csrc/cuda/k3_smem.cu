@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
   for (int i = tid; i < a.nsteps; i += kNT) ov[i] = a.overlap[i];
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
+  const long long off = a.ctrl->offset;
   const double tol = a.ctrl->tol, den = a.ctrl->den;
   if (tid == 0) s_stop = maxs <= 0;
   __syncthreads();
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
       __syncthreads();
     }
     sweep++;
-    const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
+    const bool due = mode != POBK_STOP_NONE && (((sweep + off) % every) == 0 || sweep >= maxs);
     if (due) {
       double loc = 0.0;
       if (mode == POBK_STOP_RSE) {
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
   if (tid == 0) x[a.m] = 0.0;  // the zero slot of the ELL padding (never written)
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
+  const long long off = a.ctrl->offset;
   const double tol = a.ctrl->tol, den = a.ctrl->den;
   __syncthreads();
   // stop test value = sqrt(tot)/sqrt(den) < tol; above cut_hi it cannot hold
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
       __syncthreads();
     }
     sweep++;
-    const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
+    const bool due = mode != POBK_STOP_NONE && (((sweep + off) % every) == 0 || sweep >= maxs);
     if (due) {
       double loc = 0.0;
       if (mode == POBK_STOP_RSE) {
@@ -289,7 +291,7 @@ cudaError_t launch_e(Plan& p, cudaStream_t s) {
   a.xt = p.d_xt;
   a.xst = p.d_xst;
   a.ctrl = p.d_ctrl;
-  cudaError_t e = cudaFuncSetAttribute(k3e_sweeps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+  cudaError_t e = raise_smem_limit((const void*)k3e_sweeps);
   if (e != cudaSuccess) return e;
   k3e_sweeps<<<1, kENT, p.k3_smem, s>>>(a);
   return cudaGetLastError();
@@ -312,7 +314,7 @@ cudaError_t launch(Plan& p, cudaStream_t s) {
   a.xt = p.d_xt;
   a.xst = p.d_xst;
   a.ctrl = p.d_ctrl;
-  cudaError_t e = cudaFuncSetAttribute(k3_sweeps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.k3_smem);
+  cudaError_t e = raise_smem_limit((const void*)k3_sweeps);
   if (e != cudaSuccess) return e;
   k3_sweeps<<<1, kNT, p.k3_smem, s>>>(a);
   return cudaGetLastError();

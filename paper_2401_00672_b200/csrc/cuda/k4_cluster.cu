@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kCNT, 1) k4_sweeps(K4Args a) {
   const int warp = tid >> 5, lane = tid & 31;
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
+  const long long off = a.ctrl->offset;
   const double tol = a.ctrl->tol, den = a.ctrl->den;
   cluster_sync();  // every CTA's x~ is in place before any remote access
 
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kCNT, 1) k4_sweeps(K4Args a) {
       if (a.trace && rank == 0 && tid == 0) { a.trace[4] += clock64() - tk0; a.trace[0] += 1; }
     }
     sweep++;
-    const bool due = mode != POBK_STOP_NONE && ((sweep % every) == 0 || sweep >= maxs);
+    const bool due = mode != POBK_STOP_NONE && (((sweep + off) % every) == 0 || sweep >= maxs);
     if (due) {
       double loc = 0.0;
       if (mode == POBK_STOP_RSE) {
@@ -308,7 +309,7 @@ bool k4_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t
     const K4Layout L(ent_max, slot_max, chunk, p.nsteps, blk_max);
     if (L.bytes > 227 * 1024 - 64) continue;
     // can the GPU co-schedule a cluster of C CTAs with this much shared memory?
-    if ((e = cudaFuncSetAttribute(k4_sweeps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes)) != cudaSuccess) continue;
+    if ((e = raise_smem_limit((const void*)k4_sweeps)) != cudaSuccess) continue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kCNT);
@@ -413,7 +414,7 @@ cudaError_t k4_solve(Plan& p, cudaStream_t s, long long& launches) {
   }
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k4_sweeps, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k4_sweeps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k.smem)) != cudaSuccess) return e;
+  if ((e = raise_smem_limit((const void*)k4_sweeps)) != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(k.C);
   cfg.blockDim = dim3(kCNT);

@@ -8,6 +8,9 @@
 // All reductions are two-level and deterministic: block b owns a fixed chunk, a fixed tree per
 // block, and the last block to arrive sums the block partials in index order.
 #include <cmath>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../plan.h"
 #include "common.cuh"
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kNT) k_check(Ctrl* __restrict__ c, int64_t m, 
   __shared__ int is_last;
   const long long s = c->sweeps + 1;
   const int mode = c->stop_mode;
-  const bool do_check = mode != POBK_STOP_NONE && ((s % c->check_every) == 0 || s >= c->max_sweeps);
+  const bool do_check = mode != POBK_STOP_NONE && (((s + c->offset) % c->check_every) == 0 || s >= c->max_sweeps);
   double local = 0.0;
   if (do_check) {
     if (mode == POBK_STOP_RSE) {
@@ -173,6 +176,26 @@ cudaError_t launch_permute_in(const Plan& p, const double* f, const double* x0, 
   return cudaGetLastError();
 }
 
+cudaError_t raise_smem_limit(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  // the opt-in per-block budget minus the kernel's static shared memory
+  int optin = 0;
+  cudaFuncAttributes fa;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess ||
+      (e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess)
+    return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  else (void)cudaGetLastError();  // (not sticky: leave no stale error for the caller's next check)
+  return e;
+}
+
 cudaError_t launch_permute_out(const Plan& p, double* x, cudaStream_t s, long long& launches) {
   k_permute_out<<<grid_for(p.m), kNT, 0, s>>>(p.m, p.d_perm, p.d_xt, x);
   launches++;
@@ -182,13 +205,14 @@ cudaError_t launch_permute_out(const Plan& p, double* x, cudaStream_t s, long lo
 cudaError_t launch_init_ctrl(const Plan& p, const pobk_solve_opts& o, cudaStream_t s, long long& launches) {
   Ctrl* h = p.h_ctrl;
   h->sweeps = 0;
-  h->max_sweeps = o.max_sweeps;
+  h->offset = o.sweep_offset;
+  h->max_sweeps = o.max_sweeps - o.sweep_offset;  // (this call's cap; checked >= 0 by the caller)
   h->tol = o.tol;
   h->value = NAN;
   h->den = 0.0;
   h->stop_mode = o.stop;
   h->check_every = o.check_every;
-  h->stopped = o.max_sweeps <= 0 ? 1 : 0;
+  h->stopped = h->max_sweeps <= 0 ? 1 : 0;
   h->term = POBK_TERM_MAX_SWEEPS;
   h->arrive = 0;
   h->pad = 0;

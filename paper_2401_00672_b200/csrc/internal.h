@@ -54,6 +54,8 @@ struct Ctrl {
   int term;                // POBK_TERM_*
   unsigned int arrive;     // last-block-done counter for the check reductions
   unsigned int pad;
+  long long offset;        // sweeps done before this call (resume numbering): check when
+                           // (offset + sweep) % check_every == 0
 };
 
 }  // namespace pobk

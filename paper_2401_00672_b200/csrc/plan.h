@@ -79,6 +79,11 @@ struct Plan {
 constexpr int kMaxReduceBlocks = 296;
 
 // cuda/vec_kernels.cu
+// Raise a kernel's dynamic shared-memory limit to the whole per-CTA budget (the device's opt-in
+// maximum, 227 KB on B200, minus the kernel's static shared memory), once per
+// (kernel, device), never lowering it: changing the attribute while another host thread or lane
+// launches the kernel can fail or serialise those launches (thread-safe).
+cudaError_t raise_smem_limit(const void* fn);
 // f (user frame) -> fs (storage order); x0, xstar (user frame) -> xt, xst (RCM frame); any input may be NULL
 cudaError_t launch_permute_in(const Plan& p, const double* f, const double* x0, const double* xstar, double* fs,
                               double* xt, double* xst, cudaStream_t s, long long& launches);
@@ -107,6 +112,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
 struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; };
 bool k2_stats(const Plan& p, K2Stats& st);
+bool k2_relres_ok(const Plan& p);
 void k2_free(Plan& p);
 
 }  // namespace pobk

@@ -15,7 +15,8 @@ import math
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard", "row_range", "max_over_ranks", "sum_over_ranks", "gather_objects", "sharded_residual_norm"]
+__all__ = ["shard", "row_range", "max_over_ranks", "sum_over_ranks", "gather_objects", "sharded_residual_norm",
+           "system_report", "gather_reports"]
 
 
 def shard(n_items: int, world: int, rank: int) -> list[int]:
@@ -61,3 +62,21 @@ def gather_objects(obj) -> list:
 def sharded_residual_norm(local_sumsq: float, device="cpu") -> float:
     """||f - Ax||_2 from every rank's sum over its own rows (pobk_residual_sumsq_rows)."""
     return math.sqrt(sum_over_ranks(local_sumsq, device))
+
+
+def system_report(system_id: int, nnz: int, rep) -> dict:
+    """One system's solve as reported by pobk_solve / pobk_solve_batch (pobk_report), reduced to
+    what the run summary keeps: id, stored nonzeros, sweeps, termination, final stop value."""
+    d = rep.as_dict() if hasattr(rep, "as_dict") else dict(rep)
+    return {"id": int(system_id), "nnz": int(nnz), "sweeps": int(d["sweeps"]), "termination": d["termination"],
+            "final": float(d["final_value"])}
+
+
+def gather_reports(local: list[dict], seconds: float, device="cpu") -> dict:
+    """C1: every rank's per-system reports gathered to every rank, the elapsed time
+    as the max over ranks, and the whole job's nnz-updates (sum of nnz x sweeps over all systems)."""
+    per_rank = gather_objects({"rank": dist.get_rank() if dist.is_initialized() else 0, "systems": local})
+    t = max_over_ranks(seconds, device)
+    updates = sum(r["nnz"] * r["sweeps"] for pr in per_rank for r in pr["systems"])
+    return {"ranks": per_rank, "seconds": t, "nnz_updates": float(updates),
+            "systems": sum(len(pr["systems"]) for pr in per_rank)}

@@ -338,3 +338,182 @@ def test_k3_layouts_bitwise_equal(env, name, n, monkeypatch):
     assert np.array_equal(outs[0], O.run_sweeps(pre, s.f, 17))
     assert np.array_equal(outs[0], outs[2])
     assert abs(outs[1] - outs[3]) <= 1
+
+
+# ---------------------------------------------------------------- the bench's own stopping points
+@pytest.mark.slow
+def test_config4_stop_sweep_bench_point(env):
+    """geoknn_1m at full size, in the bench's launch configuration (auto kernel -> K2), to the
+    bench's stopping point RSE < 0.1 (PAPER.md:364-365 rule, R2): the same stop sweep
+    +-1 as the oracle, the same final RSE to 1e-9, and -- at equal sweeps -- the oracle's iterates."""
+    pk, torch = env
+    s = gen.make("geoknn_1m")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, s.x_star, tol=0.1, pre=pre)
+    assert ref.termination == O.TERM_CONVERGED
+    plan = pk.Plan.from_system(s)
+    assert plan.layout_stats()["kernel"] == "wavefront"
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=0.1)
+    assert rep.termination == 0 and abs(rep.sweeps - ref.sweeps) <= 1, (rep.sweeps, ref.sweeps)
+    assert abs(rep.final_value - ref.value) <= 1e-9 * ref.value
+    if rep.sweeps == ref.sweeps:
+        assert _rel(x.cpu().numpy(), ref.x) <= REL
+
+
+@pytest.mark.slow
+def test_config5_stop_sweep_bench_point(env):
+    """Config 5 systems 0 and 63 at full size, in the bench's launch configuration (one
+    pobk_solve_batch call, half-GPU K2 tilings on concurrent lanes), to RSE < 0.1: each system's
+    stop sweep +-1 and final RSE (1e-9) against the oracle's own solve of that system."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b) for b in (0, 63)]
+    tr = pk.half_gpu_tile_rows(systems[0].m)
+    plans = [pk.Plan.from_system(s, tile_rows=tr) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = pk.solve_batch(plans, [_dev(torch, s.f) for s in systems], xs, [_dev(torch, s.x_star) for s in systems], tol=0.1)
+    for s, x, r in zip(systems, xs, reps):
+        ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, s.x_star, tol=0.1)
+        assert ref.termination == O.TERM_CONVERGED and r.termination == 0
+        assert abs(r.sweeps - ref.sweeps) <= 1, (r.sweeps, ref.sweeps)
+        assert abs(r.final_value - ref.value) <= 1e-9 * ref.value
+        if r.sweeps == ref.sweeps:
+            assert _rel(x.cpu().numpy(), ref.x) <= REL
+
+
+@pytest.mark.parametrize("kernel,name,n", [("launch", "lap2d5_32", None), ("smem", "lap2d5_32", None),
+                                           ("wavefront", "lap3d7_64", 24), ("cluster", "randband_20k", 3000)])
+def test_nonfinite_termination(env, kernel, name, n):
+    """O8 (PAPER.md:366 records non-convergence): a non-finite RSE ends the solve
+    with POBK_TERM_NONFINITE at the sweep it first appears, as in the oracle (f with an inf)."""
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    f = s.f.copy()
+    f[7] = np.inf
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, f, s.x_star, tol=1e-6, max_sweeps=50)
+    assert ref.termination == O.TERM_NONFINITE
+    try:
+        plan = pk.Plan.from_system(s, kernel=kernel)
+    except pk.PobkError as e:
+        pytest.skip(f"{kernel} not applicable: {e}")
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, f), x, _dev(torch, s.x_star), tol=1e-6, max_sweeps=50)
+    assert rep.termination == 2 and rep.sweeps == ref.sweeps, (rep.as_dict(), ref.sweeps)
+
+
+@pytest.mark.parametrize("thr", [0.05])
+def test_thr_positive_parity_20k(env, thr):
+    """Overlapping categories (thr > 0) at m = 20,000 (config 2) on K1: the same
+    thresholded partition as the oracle, iterates within 1e-9 after 25 sweeps and the same RSE
+    stop sweep +-1 (fp64 atomics: order-dependent rounding, so not bitwise)."""
+    pk, torch = env
+    s = gen.make("randband_20k")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data, thr=thr)
+    assert pre.overlap.any() and pre.nsteps < O.preprocess(s.m, s.indptr, s.indices, s.data).nsteps
+    plan = pk.Plan.from_system(s, thr=thr)
+    colour, cat_ptr, cat_rows = plan.partition()
+    assert np.array_equal(colour, pre.color) and np.array_equal(cat_rows, pre.cat_rows)
+    _, x, _ = _run(env, s, 25, plan=plan)
+    assert _rel(x, O.run_sweeps(pre, s.f, 25)) <= REL
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, s.x_star, tol=1e-6, pre=pre)
+    xx = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), xx, _dev(torch, s.x_star), tol=1e-6)
+    assert rep.termination == ref.termination and abs(rep.sweeps - ref.sweeps) <= 1
+
+
+# ---------------------------------------------------------------- RELRES inside K2, resume, batch contract
+@pytest.mark.slow
+def test_relres_on_wavefront_config4(env):
+    """RELRES stop (||f~ - A~x~||/||f~||) evaluated inside K2 (residual pass over each
+    tile's stream, fixed-order reductions) at full config-4 size: the solve stays on the wavefront
+    kernel and stops within +-1 sweep of the oracle's O8 rule (PAPER.md:364 strict '<'), with the
+    same RELRES value to 1e-9 when the sweeps agree."""
+    pk, torch = env
+    s = gen.make("geoknn_1m")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    tr = O.solve(s.m, s.indptr, s.indices, s.data, s.f, stop="relres", tol=0.0, max_sweeps=30, keep_trace=True, pre=pre)
+    tol = float(tr.trace[24]) * (1 + 1e-9)   # the oracle stops at sweep 25 (trace decreasing there)
+    assert tr.trace[23] > tol
+    ref = O.solve(s.m, s.indptr, s.indices, s.data, s.f, stop="relres", tol=tol, pre=pre)
+    plan = pk.Plan.from_system(s)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, None, tol=tol, stop="relres")
+    assert rep.kernel == 2, rep.as_dict()  # POBK_KERNEL_WAVEFRONT
+    assert rep.termination == 0 and abs(rep.sweeps - ref.sweeps) <= 1, (rep.sweeps, ref.sweeps)
+    assert np.isnan(rep.final_rse) and rep.final_relres == rep.final_value
+    if rep.sweeps == ref.sweeps:
+        assert abs(rep.final_value - ref.value) <= 1e-9 * ref.value
+
+
+@pytest.mark.parametrize("name,n,kernel", [("lap3d7_64", 24, "wavefront"), ("lap2d5_32", None, "smem"),
+                                           ("randband_20k", 4000, "launch")])
+def test_relres_fixed_count_value(env, name, n, kernel):
+    """RELRES after a fixed sweep count (tol 0, cap N: the check at the cap reports the value) on
+    each kernel family equals the oracle's relres of the oracle's iterate to 1e-12."""
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    plan = pk.Plan.from_system(s, kernel=kernel)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, None, tol=0.0, max_sweeps=9, stop="relres")
+    assert rep.sweeps == 9 and rep.termination == 1
+    xr = O.run_sweeps(pre, s.f, 9)
+    v = O.relres(pre, O.permute_vector(s.f, pre.perm), O.permute_vector(xr, pre.perm))
+    assert abs(rep.final_relres - v) <= 1e-12 * v
+
+
+@pytest.mark.parametrize("name,n,kernel", [("lap3d7_64", 24, "wavefront"), ("lap2d5_32", None, "smem"),
+                                           ("lap2d5_32", None, "launch")])
+def test_sweep_offset_resume(env, name, n, kernel):
+    """Resume (SURVEY §5 checkpoint/resume, §8b sweep_offset): 7 sweeps, then a second call from
+    that x with sweep_offset = 7 and the same total cap, equals 12 uninterrupted sweeps bitwise;
+    checks fall on the same sweep numbers (check_every = 5: a loose tol stops at total sweep 10)."""
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    plan = pk.Plan.from_system(s, kernel=kernel)
+    f, xs = _dev(torch, s.f), _dev(torch, s.x_star)
+    x12 = _dev(torch, np.zeros(s.m))
+    plan.solve(f, x12, xs, max_sweeps=12, stop="none")
+    x = _dev(torch, np.zeros(s.m))
+    r1 = plan.solve(f, x, xs, max_sweeps=7, stop="none")
+    r2 = plan.solve(f, x, xs, max_sweeps=12, stop="none", sweep_offset=7)
+    assert (r1.sweeps, r2.sweeps, r2.sweeps_total) == (7, 5, 12)
+    assert np.array_equal(x.cpu().numpy(), x12.cpu().numpy())
+    x = _dev(torch, np.zeros(s.m))
+    plan.solve(f, x, xs, max_sweeps=7, stop="none")
+    r3 = plan.solve(f, x, xs, tol=10.0, check_every=5, sweep_offset=7)
+    assert r3.termination == 0 and r3.sweeps == 3 and r3.sweeps_total == 10
+    r4 = plan.solve(f, x, xs, max_sweeps=7, sweep_offset=9)   # offset past the cap: nothing to do
+    assert r4.sweeps == 0 and r4.sweeps_total == 9
+
+
+def test_batch_duplicate_plan_and_bad_args(env):
+    """pobk_solve_batch contract: a batch naming one plan twice gives each system its own
+    back-to-back result (a plan is not re-entrant); a bad argument in any system fails the call
+    before anything is enqueued (x of the other systems untouched)."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b, n=160) for b in range(2)]
+    tr = pk.half_gpu_tile_rows(systems[0].m)
+    p = pk.Plan.from_system(systems[0], kernel="wavefront", tile_rows=tr)
+    f = _dev(torch, systems[0].f)
+    xs = [_dev(torch, np.zeros(systems[0].m)) for _ in range(2)]
+    reps = pk.solve_batch([p, p], [f, f], xs, None, max_sweeps=15, stop="none")
+    x1 = _dev(torch, np.zeros(systems[0].m))
+    p.solve(f, x1, None, max_sweeps=15, stop="none")
+    assert all(r.sweeps == 15 for r in reps)
+    assert np.array_equal(xs[0].cpu().numpy(), x1.cpu().numpy()) and np.array_equal(xs[1].cpu().numpy(), x1.cpu().numpy())
+    q = pk.Plan.from_system(systems[1], kernel="wavefront", tile_rows=tr)
+    x0 = [_dev(torch, np.zeros(s.m)) for s in systems]
+    with pytest.raises(pk.PobkError):  # system 1: RSE stop without x*
+        import ctypes
+        L = pk._lib
+        H = (ctypes.c_void_p * 2)(p._h.value, q._h.value)
+        F = (ctypes.c_void_p * 2)(f.data_ptr(), _dev(torch, systems[1].f).data_ptr())
+        X = (ctypes.c_void_p * 2)(x0[0].data_ptr(), x0[1].data_ptr())
+        XS = (ctypes.c_void_p * 2)(_dev(torch, systems[0].x_star).data_ptr(), None)
+        reps = (L.Report * 2)()
+        o = pk._solve_opts(1e-3, 100, "rse", 1)
+        L.check(L.lib.pobk_solve_batch(H, 2, ctypes.cast(F, ctypes.c_void_p), ctypes.cast(X, ctypes.c_void_p),
+                                       ctypes.cast(XS, ctypes.c_void_p), ctypes.byref(o), None, ctypes.cast(reps, ctypes.c_void_p)))
+    torch.cuda.synchronize()
+    assert not x0[0].any().item()

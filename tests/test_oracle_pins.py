@@ -429,6 +429,50 @@ def test_rse_closed_forms():
     assert O.rse(np.array([3.0, 9.0]), xs) == 1.0
 
 
+def _relres_pre(A, reorder):
+    A = gen.canonical(sp.csr_matrix(A))
+    return A, O.preprocess(A.shape[0], A.indptr, A.indices, A.data, reorder=reorder)
+
+
+@pytest.mark.parametrize("reorder", [0, 1])
+def test_relres_closed_forms(reorder):
+    """RELRES = ||f - A x||_2 / ||f||_2 (the residual stop of SURVEY Z13, beside the RSE of
+    PAPER.md:365), evaluated by the oracle in the RCM frame.  Pins, each failing a plausible
+    slip: x = 0 gives exactly 1 (a missing normalisation gives ||f||); a hand-computed 2x2 value
+    sqrt(5)/5 for A = [[2,1],[0,3]], f = (3,4), x = (0,1) (r = (2,1)), which a missing sqrt (0.2),
+    a squared numerator (1.0), a missing ||f|| (sqrt 5) or a swapped operand (A^T x: r = (3,0),
+    0.6) all miss; the exact solution gives 0."""
+    A, pre = _relres_pre(np.array([[2.0, 1.0], [0.0, 3.0]]), reorder)
+    f = np.array([3.0, 4.0])
+    f_t = O.permute_vector(f, pre.perm)
+    assert O.relres(pre, f_t, np.zeros(2)) == 1.0
+    x = np.array([0.0, 1.0])
+    v = O.relres(pre, f_t, O.permute_vector(x, pre.perm))
+    assert abs(v - np.sqrt(5.0) / 5.0) <= 1e-16
+    assert O.relres(pre, f_t, O.permute_vector(np.array([5.0 / 6.0, 4.0 / 3.0]), pre.perm)) <= 1e-15
+    # the user-frame residual norm of the same point (SPEC.md:55-58)
+    assert abs(O.residual_norm(2, A.indptr, A.indices, A.data, f, x) - np.sqrt(5.0)) <= 1e-15
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_relres_frame_invariant_and_scale_free(seed):
+    """RELRES does not depend on the frame (P^T P = E, Eq 4.1) and is invariant under
+    f -> c f, x -> c x (homogeneous of degree 0): a reordering of the sum or a missing ||f||
+    normalisation breaks one of the two."""
+    rng = np.random.default_rng(seed)
+    A = gen.scramble(gen.random_banded(40, 500 + seed, half=3), 600 + seed)
+    A = gen.canonical(A)
+    f = rng.standard_normal(40)
+    x = rng.standard_normal(40)
+    pre0 = O.preprocess(40, A.indptr, A.indices, A.data, reorder=0)
+    pre1 = O.preprocess(40, A.indptr, A.indices, A.data, reorder=1)
+    v0 = O.relres(pre0, f, x)
+    v1 = O.relres(pre1, O.permute_vector(f, pre1.perm), O.permute_vector(x, pre1.perm))
+    ref = np.linalg.norm(f - A @ x) / np.linalg.norm(f)
+    assert abs(v0 - ref) <= 1e-13 * ref and abs(v1 - ref) <= 1e-13 * ref
+    assert abs(O.relres(pre0, 8.0 * f, 8.0 * x) - v0) <= 1e-15 * v0  # (8: exact power-of-two scaling)
+
+
 def test_stop_is_strict_less_than():
     """PAPER.md:364 'less than 1e-6': value == tol does not stop."""
     s = gen.make("lap2d5_32")

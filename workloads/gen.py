@@ -205,16 +205,18 @@ def random_pattern_graph(m: int, seed: int, p: float) -> sp.csr_matrix:
 
 # ---------------------------------------------------------------- configs
 
-# name -> (builder(system_id, scale) -> csr, scramble seed(system_id), x* seed(system_id))
+# name -> (builder(system_id, scale) -> csr, scramble seed(system_id), x* seed(system_id)).
+# Single-system configs: system b > 0 (a replica on rank b of a multi-GPU run) keeps the matrix
+# and scramble and draws its own x* (seed + 1000 b); b = 0 is the BASELINE config itself.
 CONFIGS = {
     # BASELINE.json configs[0]
-    "lap2d5_32": dict(build=lambda b, n=32: lap2d5(n), scramble=lambda b: 101, xstar=lambda b: 201, n=32),
+    "lap2d5_32": dict(build=lambda b, n=32: lap2d5(n), scramble=lambda b: 101, xstar=lambda b: 201 + 1000 * b, n=32),
     # BASELINE.json configs[1]
-    "randband_20k": dict(build=lambda b, n=20000: randband(n, 302), scramble=lambda b: 102, xstar=lambda b: 202, n=20000),
+    "randband_20k": dict(build=lambda b, n=20000: randband(n, 302), scramble=lambda b: 102, xstar=lambda b: 202 + 1000 * b, n=20000),
     # BASELINE.json configs[2]
-    "lap3d7_64": dict(build=lambda b, n=64: lap3d7(n, 303), scramble=lambda b: 103, xstar=lambda b: 203, n=64),
+    "lap3d7_64": dict(build=lambda b, n=64: lap3d7(n, 303), scramble=lambda b: 103, xstar=lambda b: 203 + 1000 * b, n=64),
     # BASELINE.json configs[3]
-    "geoknn_1m": dict(build=lambda b, n=1000000: geoknn(n, 304), scramble=lambda b: 104, xstar=lambda b: 204, n=1000000),
+    "geoknn_1m": dict(build=lambda b, n=1000000: geoknn(n, 304), scramble=lambda b: 104, xstar=lambda b: 204 + 1000 * b, n=1000000),
     # BASELINE.json configs[4]: 64 independent systems b = 0..63
     "batch9pt_1024": dict(build=lambda b, n=1024: box9(n), scramble=lambda b: 1050 + b, xstar=lambda b: 2050 + b, n=1024),
 }
