@@ -72,7 +72,8 @@ enum {
   POBK_KERNEL_LAUNCH = 1,    /* K1: one launch per category step, device-driven CUDA-graph loop */
   POBK_KERNEL_WAVEFRONT = 2, /* K2: persistent tiled wavefront, x~ tile-private in shared memory */
   POBK_KERNEL_SMEM = 3,      /* K3: one CTA, whole system resident in shared memory */
-  POBK_KERNEL_CLUSTER = 4    /* K4: one thread-block cluster, system in distributed shared memory */
+  POBK_KERNEL_CLUSTER = 4,   /* K4: one thread-block cluster, system in distributed shared memory */
+  POBK_KERNEL_BLOCKS = 5     /* K5: the paper-literal k-block iteration (pobk_blocks_preprocess only) */
 };
 
 typedef struct {
@@ -188,6 +189,35 @@ pobk_status pobk_residual_norm(pobk_plan_t plan, const double* f_dev, const doub
  * all-reduce SUM, then sqrt). */
 pobk_status pobk_residual_sumsq_rows(pobk_plan_t plan, int64_t row_begin, int64_t row_end, const double* f_dev,
                                      const double* x_dev, void* stream, double* out);
+
+/* ---- The paper-literal variant: k uniform row blocks (Alg 5 as written).
+ * Steps: RCM; blocks 1..k-1 take floor(m/k) consecutive rows of A~, block k the rest
+ * (P:207); the centroid cosine table C(i,j) = |(A-bar_i, A-bar_j)| / (||A-bar_i|| ||A-bar_j||)
+ * (absolute value: DESIGN.md §3); C(i,j) < thr counts as orthogonal and each unused block
+ * pairs with the first unused later block orthogonal to it (Oclass pairs), the rest is Nclass
+ * (P:220).  One iteration applies every pair (tau1 then tau2) and then every Nclass block, each
+ * as the block projection x~ += A_tau^+ (f~_tau - A_tau x~) (Eq 3.3) with
+ * A_tau^+ = A_tau^T (A_tau A_tau^T)^-1 (Lemma 1: full-row-rank blocks; a
+ * rank-deficient block fails with POBK_ERR_ARG).  The dense Gram inverses are built once at
+ * preprocessing (8 b^2 bytes per block of b rows; blocks above 20,000 rows are refused).
+ * The returned plan is solved with pobk_solve / pobk_solve_host (kernel POBK_KERNEL_BLOCKS);
+ * plan_get_partition reports colour = block id, cat_ptr = block boundaries. */
+typedef struct {
+  int32_t k;       /* number of blocks, 1 <= k <= m (the paper uses k < 20) */
+  double thr;      /* orthogonality threshold on C, 0 <= thr < 1 */
+  int32_t reorder; /* 1 (default): RCM; 0: identity */
+} pobk_blocks_opts;
+
+pobk_status pobk_blocks_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                   const pobk_blocks_opts* opts, int device, pobk_plan_t* out);
+
+/* The k-block layout: k; block_ptr[k+1] (RCM-frame row boundaries); cos_table[k*k] (row-major
+ * C); pairs[2*npairs] (Oclass, 0-based block ids, in iteration order); nclass[nnclass]; the
+ * Definition 1-2 diagnostics zn (orthogonality proportion) and nn (non-orthogonality severity),
+ * P:512-516, on the table with entries < thr set to 0.  Array outputs may be NULL; pairs and
+ * nclass need room for k entries. */
+pobk_status pobk_blocks_info(pobk_plan_t plan, int32_t* k, int64_t* block_ptr, double* cos_table, int32_t* pairs,
+                             int32_t* npairs, int32_t* nclass, int32_t* nnclass, double* zn, double* nn);
 
 void pobk_plan_destroy(pobk_plan_t plan);
 

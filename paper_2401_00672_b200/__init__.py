@@ -82,6 +82,41 @@ class Plan:
     def from_system(cls, system, **kw) -> "Plan":
         return cls.from_csr(system.m, system.indptr, system.indices, system.data, **kw)
 
+    @classmethod
+    def from_csr_blocks(cls, m: int, indptr, indices, data, k: int, thr: float, reorder: int = 1,
+                        device: int | None = None) -> "Plan":
+        """The paper-literal variant (pobk_blocks_preprocess): k uniform row blocks, centroid
+        cosine table, Oclass pairs / Nclass (Alg 5 as written); solved with Plan.solve."""
+        if device is None:
+            device = _torch().cuda.current_device()
+        ip = L.as_host(indptr, np.int64)
+        ix = L.as_host(indices, np.int32)
+        vd = L.as_host(data, np.float64)
+        o = L.BlocksOpts(int(k), float(thr), int(reorder))
+        h = ctypes.c_void_p()
+        L.check(L.lib.pobk_blocks_preprocess(int(m), L.ptr(ip), L.ptr(ix), L.ptr(vd), ctypes.byref(o), int(device),
+                                             ctypes.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def from_system_blocks(cls, system, **kw) -> "Plan":
+        return cls.from_csr_blocks(system.m, system.indptr, system.indices, system.data, **kw)
+
+    def blocks_info(self) -> dict:
+        """k, block boundaries, the cosine table C, Oclass pairs, Nclass blocks, zn, nn."""
+        k = ctypes.c_int32()
+        L.check(L.lib.pobk_blocks_info(self._h, ctypes.byref(k), None, None, None, None, None, None, None, None))
+        k = k.value
+        ptr = np.empty(k + 1, np.int64)
+        C = np.empty((k, k), np.float64)
+        pairs = np.empty(2 * k, np.int32)
+        ncl = np.empty(k, np.int32)
+        npair, nn_, zn, nn = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+        L.check(L.lib.pobk_blocks_info(self._h, None, L.ptr(ptr), L.ptr(C), L.ptr(pairs), ctypes.byref(npair), L.ptr(ncl),
+                                       ctypes.byref(nn_), ctypes.byref(zn), ctypes.byref(nn)))
+        return {"k": k, "ptr": ptr, "C": C, "pairs": [tuple(map(int, pairs[2 * i:2 * i + 2])) for i in range(npair.value)],
+                "nclass": ncl[:nn_.value].tolist(), "zn": zn.value, "nn": nn.value}
+
     # ------------------------------------------------------------ queries
     def perm(self) -> np.ndarray:
         out = np.empty(self.m, dtype=np.int32)

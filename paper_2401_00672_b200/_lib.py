@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libpobk.so")
 OK, ERR_ARG, ERR_BAD_CSR, ERR_ZERO_ROW, ERR_UNSTABLE_THR, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(8)
 TERM_CONVERGED, TERM_MAX_SWEEPS, TERM_NONFINITE = 0, 1, 2
 STOP = {"rse": 0, "relres": 1, "none": 2}
-KERNEL = {"auto": 0, "launch": 1, "wavefront": 2, "smem": 3, "cluster": 4}
+KERNEL = {"auto": 0, "launch": 1, "wavefront": 2, "smem": 3, "cluster": 4, "blocks": 5}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 TERM_NAME = {TERM_CONVERGED: "converged", TERM_MAX_SWEEPS: "max_sweeps", TERM_NONFINITE: "nonfinite"}
 
@@ -30,6 +30,10 @@ class PreprocessOpts(ctypes.Structure):
 class SolveOpts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_sweeps", ctypes.c_int64), ("stop", ctypes.c_int32),
                 ("check_every", ctypes.c_int32), ("sweep_offset", ctypes.c_int64)]
+
+
+class BlocksOpts(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("thr", ctypes.c_double), ("reorder", ctypes.c_int32)]
 
 
 class LayoutStats(ctypes.Structure):
@@ -81,6 +85,9 @@ SIGNATURES = {
     "pobk_solve_batch": (I32, [ctypes.POINTER(P), I32, P, P, P, ctypes.POINTER(SolveOpts), P, P]),
     "pobk_residual_norm": (I32, [P, P, P, P, ctypes.POINTER(F64)]),
     "pobk_residual_sumsq_rows": (I32, [P, I64, I64, P, P, P, ctypes.POINTER(F64)]),
+    "pobk_blocks_preprocess": (I32, [I64, P, P, P, ctypes.POINTER(BlocksOpts), ctypes.c_int, ctypes.POINTER(P)]),
+    "pobk_blocks_info": (I32, [P, ctypes.POINTER(I32), P, P, P, ctypes.POINTER(I32), P, ctypes.POINTER(I32),
+                               ctypes.POINTER(F64), ctypes.POINTER(F64)]),
     "pobk_plan_destroy": (None, [P]),
     "pobk_last_error": (ctypes.c_char_p, []),
     "pobk_abi_version": (I32, []),

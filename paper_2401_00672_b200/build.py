@@ -20,12 +20,14 @@ COMMON = [f"-DPOBK_K2_MAXJ={os.environ.get('POBK_K2_MAXJ', '24')}", "-O3", "-std
 
 SOURCES = [
     "host/preprocess.cpp",
+    "host/blocks.cpp",
     "capi.cpp",
     "cuda/vec_kernels.cu",
     "cuda/k1_launch.cu",
     "cuda/k3_smem.cu",
     "cuda/k2_wavefront.cu",
     "cuda/k4_cluster.cu",
+    "cuda/k5_blocks.cu",
 ]
 HEADERS = ["internal.h", "plan.h", "cuda/common.cuh", "../../include/pobk.h"]
 

@@ -65,6 +65,7 @@ void destroy_plan(Plan* p) {
     DeviceGuard g(p->device);
     if (p->k2) k2_free(*p);
     if (p->k4) k4_free(*p);
+    if (p->k5) k5_free(*p);
     if (p->k1_exec) cudaGraphExecDestroy(p->k1_exec);
     if (p->k1_graph) cudaGraphDestroy(p->k1_graph);
     for (void* a : p->allocations) cudaFree(a);
@@ -135,6 +136,12 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
     if (!k2_build(p, At, nrm2, tile_rows, why)) return fail(POBK_ERR_ARG, "kernel=WAVEFRONT unavailable: " + why);
   } else if (req == POBK_KERNEL_CLUSTER) {
     if (!k4_build(p, rp, col, val, why)) return fail(POBK_ERR_ARG, "kernel=CLUSTER unavailable: " + why);
+  } else if (req == POBK_KERNEL_BLOCKS) {  // the k-block variant: Gram inverses + K5 layout
+    std::vector<std::vector<double>> ginv;
+    Error err;
+    if (!block_gram_inverses(At, p.blocks_host, ginv, err)) return fail(err.code, err.msg);
+    if (!k5_build(p, At, std::move(p.blocks_host), std::move(ginv), why)) return fail(POBK_ERR_CUDA, why);
+    p.blocks_host = BlockLayout();
   } else if (req == POBK_KERNEL_AUTO) {
     // K3 (one CTA) when the system fits one CTA's shared memory, else the K2 wavefront from
     // m >= 4096, else K1 (K4, one cluster, is explicit-only: slower than K2 where both apply)
@@ -163,6 +170,7 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
       case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
       case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, f, s, launches)); break;
       case POBK_KERNEL_CLUSTER: CUDA_TRY(k4_solve(p, s, launches)); break;
+      case POBK_KERNEL_BLOCKS: CUDA_TRY(k5_solve(p, s, launches)); break;
       default: CUDA_TRY(k1_solve(p, s, launches)); break;
     }
   }
@@ -187,6 +195,7 @@ pobk_status solve_finish(Plan& p, const pobk_solve_opts& o, pobk_report* rep) {
   const Ctrl& c = *p.h_ctrl;
   const bool ran = o.max_sweeps - o.sweep_offset > 0;
   if (used == POBK_KERNEL_LAUNCH && ran) launches += c.sweeps * p.k1_nodes_per_sweep;
+  if (used == POBK_KERNEL_BLOCKS && ran) launches += c.sweeps * k5_nodes_per_sweep(p);
   if (rep) {
     rep->sweeps = ran ? c.sweeps : 0;
     rep->termination = c.term;
@@ -312,6 +321,98 @@ pobk_status pobk_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* co
   } catch (const std::exception& e) {
     return fail(POBK_ERR_ARG, std::string("preprocessing failed: ") + e.what());
   }
+}
+
+pobk_status pobk_blocks_preprocess(int64_t m, const int64_t* row_ptr, const int32_t* col, const double* val,
+                                   const pobk_blocks_opts* opts, int device, pobk_plan_t* out) {
+  g_err.clear();
+  if (!out) return fail(POBK_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!opts) return fail(POBK_ERR_ARG, "opts is NULL (k has no default)");
+  if (device < -1) return fail(POBK_ERR_ARG, "device must be >= -1");
+  try {
+    auto t0 = std::chrono::steady_clock::now();
+    HostCSR A;
+    Error err;
+    if (!canonicalize(m, row_ptr, col, val, A, err)) return fail(err.code, err.msg);
+    Plan* p = new pobk_plan_s();
+    p->device = device;
+    p->m = m;
+    p->nnz = A.nnz();
+    p->thr = opts->thr;
+    p->kernel = POBK_KERNEL_BLOCKS;
+    p->bw_before = bandwidth(A);
+    if (opts->reorder) rcm_order(A, p->perm);
+    else {
+      p->perm.resize(m);
+      for (int64_t i = 0; i < m; i++) p->perm[i] = (int32_t)i;
+    }
+    HostCSR At;
+    permute_symmetric(A, p->perm, At);
+    { HostCSR().ptr.swap(A.ptr); std::vector<int32_t>().swap(A.col); std::vector<double>().swap(A.val); }
+    p->bw_after = bandwidth(At);
+    if (!block_layout(At, opts->k, opts->thr, p->blocks_host, err)) {
+      destroy_plan(p);
+      return fail(err.code, err.msg);
+    }
+    const BlockLayout& L = p->blocks_host;
+    // storage order = RCM order; "categories" = the blocks (colour = block id)
+    p->colour.assign(m, 0);
+    p->sched.step_ptr.assign(L.k + 1, 0);
+    for (int32_t b = 0; b < L.k; b++) {
+      p->sched.step_ptr[b + 1] = (int32_t)L.ptr[b + 1];
+      for (int64_t r = L.ptr[b]; r < L.ptr[b + 1]; r++) p->colour[r] = b;
+    }
+    p->sched.rows.resize(m);
+    for (int64_t i = 0; i < m; i++) p->sched.rows[i] = (int32_t)i;
+    p->sched.n_oclass = (int32_t)(2 * L.pairs.size());
+    p->sched.overlap.assign(L.k, 0);
+    p->nsteps = L.k;
+    p->n_oclass = p->sched.n_oclass;
+    if (device >= 0) {
+      int64_t bmax = 0;
+      for (int32_t b = 0; b < L.k; b++) bmax = std::max<int64_t>(bmax, L.ptr[b + 1] - L.ptr[b]);
+      if (bmax > 20000) {
+        destroy_plan(p);
+        return fail(POBK_ERR_ARG, "blocks of " + std::to_string(bmax) + " rows: the k-block path keeps a dense Gram "
+                                  "inverse per block and takes blocks of <= 20,000 rows (raise k)");
+      }
+      std::vector<double> nrm2;
+      row_sqnorms(At, nrm2);
+      pobk_status st = build_device(*p, At, nrm2, 0);
+      if (st != POBK_OK) {
+        std::string keep = g_err;
+        destroy_plan(p);
+        g_err = keep;
+        return st;
+      }
+    }
+    p->prep_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = static_cast<pobk_plan_s*>(p);
+    return POBK_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(POBK_ERR_OOM, "host allocation failed during preprocessing");
+  } catch (const std::exception& e) {
+    return fail(POBK_ERR_ARG, std::string("preprocessing failed: ") + e.what());
+  }
+}
+
+pobk_status pobk_blocks_info(pobk_plan_t p, int32_t* k, int64_t* block_ptr, double* cos_table, int32_t* pairs,
+                             int32_t* npairs, int32_t* nclass, int32_t* nnclass, double* zn, double* nn) {
+  if (!p) return fail(POBK_ERR_ARG, "plan is NULL");
+  const BlockLayout* L = p->k5 ? k5_layout(*p) : (p->blocks_host.k > 0 ? &p->blocks_host : nullptr);
+  if (!L) return fail(POBK_ERR_ARG, "not a k-block plan (pobk_blocks_preprocess)");
+  if (k) *k = L->k;
+  if (block_ptr) std::memcpy(block_ptr, L->ptr.data(), L->ptr.size() * sizeof(int64_t));
+  if (cos_table) std::memcpy(cos_table, L->cos.data(), L->cos.size() * sizeof(double));
+  if (pairs)
+    for (size_t i = 0; i < L->pairs.size(); i++) { pairs[2 * i] = L->pairs[i].first; pairs[2 * i + 1] = L->pairs[i].second; }
+  if (npairs) *npairs = (int32_t)L->pairs.size();
+  if (nclass) std::memcpy(nclass, L->nclass.data(), L->nclass.size() * sizeof(int32_t));
+  if (nnclass) *nnclass = (int32_t)L->nclass.size();
+  if (zn) *zn = L->zn;
+  if (nn) *nn = L->nn;
+  return POBK_OK;
 }
 
 pobk_status pobk_plan_info(pobk_plan_t p, int64_t* m, int64_t* nnz, int32_t* nsteps, int32_t* n_oclass, int64_t* bw_before,

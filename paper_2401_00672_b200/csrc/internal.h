@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pobk.h"
@@ -39,6 +40,20 @@ struct Schedule {
 void build_schedule(const HostCSR& A, const std::vector<int32_t>& colour, bool check_overlap, Schedule& s);
 bool gershgorin_guard(const HostCSR& A, const std::vector<double>& nrm2, const std::vector<int32_t>& colour,
                       std::string& why);
+
+// host/blocks.cpp -- the paper-literal k-block variant (Alg 5 steps 2-4 with k uniform chunks).
+struct BlockLayout {
+  int32_t k = 0;
+  double thr = 0.0;
+  std::vector<int64_t> ptr;                        // [k+1] block boundaries (RCM frame)
+  std::vector<double> cos;                         // [k*k] centroid cosine table C
+  std::vector<std::pair<int32_t, int32_t>> pairs;  // Oclass: class{i} = (i, j)
+  std::vector<int32_t> nclass;                     // Nclass blocks, ascending
+  std::vector<int32_t> order;                      // one iteration: pairs (tau1, tau2), then Nclass
+  double zn = 0.0, nn = 0.0;                       // Definitions 1-2
+};
+bool block_layout(const HostCSR& At, int32_t k, double thr, BlockLayout& out, Error& err);
+bool block_gram_inverses(const HostCSR& At, const BlockLayout& L, std::vector<std::vector<double>>& ginv, Error& err);
 
 // ----------------------------------------------------------------------------- device control block
 // One per solve, in device memory.  Written by the check kernels, read back at the end.

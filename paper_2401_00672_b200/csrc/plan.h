@@ -22,6 +22,7 @@ struct DevCSR {
 
 struct K2Plan;  // cuda/k2_wavefront.cu
 struct K4Plan;  // cuda/k4_cluster.cu
+struct K5Plan;  // cuda/k5_blocks.cu
 
 struct Plan {
   int device = -1;
@@ -65,6 +66,8 @@ struct Plan {
   long long pending_launches = 0;  // solve_device -> solve_finish (batched solves)
   int pending_used = 0;
   K4Plan* k4 = nullptr;
+  K5Plan* k5 = nullptr;            // the paper-literal k-block variant (pobk_blocks_preprocess)
+  BlockLayout blocks_host;         // its layout on host-only plans (device = -1)
   size_t k3_smem = 0;
   int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps
   uint8_t* k3_overlap = nullptr;   // [nsteps]
@@ -107,6 +110,12 @@ bool k4_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t
 cudaError_t k4_solve(Plan& p, cudaStream_t s, long long& launches);
 void k4_free(Plan& p);
 int k4_cluster_size(const Plan& p);
+// cuda/k5_blocks.cu (the paper-literal k-block variant)
+bool k5_build(Plan& p, const HostCSR& At, BlockLayout&& L, std::vector<std::vector<double>>&& ginv, std::string& why);
+cudaError_t k5_solve(Plan& p, cudaStream_t s, long long& launches);
+long long k5_nodes_per_sweep(const Plan& p);
+const BlockLayout* k5_layout(const Plan& p);
+void k5_free(Plan& p);
 // cuda/k2_wavefront.cu
 bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why);
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
