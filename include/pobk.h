@@ -166,6 +166,17 @@ pobk_status pobk_solve(pobk_plan_t plan, const double* f_dev, double* x_dev, con
 pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const double* xstar,
                             const pobk_solve_opts* opts, void* stream, pobk_report* rep);
 
+/* R right-hand sides of ONE plan's matrix (Ax = f for R vectors f; the north star's
+ * "batches of ... right-hand sides"), 1 <= R <= 8, in one sweep loop: each schedule step reads
+ * every row of A~ once for all R (x~ and f~ R-interleaved), and applies Eq 1.2 to each right-hand
+ * side in the per-row contract order, so right-hand side r's iterates and stop sweep are bitwise
+ * those of its own pobk_solve.  Each right-hand side stops on its own rule (POBK_STOP_RSE, needs
+ * xstar[r]; or POBK_STOP_NONE); POBK_STOP_RELRES is refused.  Row-level plans with thr = 0 only.
+ * Arrays of R device pointers (x distinct, in/out); reps[R]; blocks until filled. */
+pobk_status pobk_solve_multi(pobk_plan_t plan, int32_t R, const double* const* f_dev, double* const* x_dev,
+                             const double* const* xstar_dev, const pobk_solve_opts* opts, void* stream,
+                             pobk_report* reps);
+
 /* Alg 5 for nb independent systems (one plan each, same device; the batched
  * configuration of the north star, one shard of a multi-GPU batch): every system stops on its
  * own rule.  All arguments are checked before anything is enqueued.

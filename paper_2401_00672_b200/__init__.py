@@ -168,6 +168,21 @@ class Plan:
                                       ctypes.byref(o), _stream(stream), ctypes.byref(rep)))
         return rep
 
+    def solve_multi(self, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse",
+                    check_every: int = 1, stream=None, sweep_offset: int = 0) -> list[Report]:
+        """pobk_solve_multi: R <= 8 right-hand sides of this plan's matrix in one sweep loop (A read
+        once per step for all of them); each stops on its own rule; bitwise the single solves."""
+        R = len(fs)
+        F = (ctypes.c_void_p * R)(*[_dev_ptr(f, "f", self.m).value for f in fs])
+        X = (ctypes.c_void_p * R)(*[_dev_ptr(x, "x", self.m).value for x in xs])
+        XS = (ctypes.c_void_p * R)(*[_dev_ptr(x, "x_star", self.m).value for x in x_stars]) if x_stars else None
+        reps = (L.Report * R)()
+        o = _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset)
+        L.check(L.lib.pobk_solve_multi(self._h, R, ctypes.cast(F, ctypes.c_void_p), ctypes.cast(X, ctypes.c_void_p),
+                                       ctypes.cast(XS, ctypes.c_void_p) if XS is not None else None, ctypes.byref(o),
+                                       _stream(stream), ctypes.cast(reps, ctypes.c_void_p)))
+        return list(reps)
+
     def residual_norm(self, f, x, stream=None) -> float:
         out = ctypes.c_double()
         L.check(L.lib.pobk_residual_norm(self._h, _dev_ptr(f, "f", self.m), _dev_ptr(x, "x", self.m), _stream(stream),

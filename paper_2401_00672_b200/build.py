@@ -24,6 +24,7 @@ SOURCES = [
     "capi.cpp",
     "cuda/vec_kernels.cu",
     "cuda/k1_launch.cu",
+    "cuda/k1_multi.cu",
     "cuda/k3_smem.cu",
     "cuda/k2_wavefront.cu",
     "cuda/k4_cluster.cu",

@@ -66,6 +66,7 @@ void destroy_plan(Plan* p) {
     if (p->k2) k2_free(*p);
     if (p->k4) k4_free(*p);
     if (p->k5) k5_free(*p);
+    if (p->multi) k1m_free(*p);
     if (p->k1_exec) cudaGraphExecDestroy(p->k1_exec);
     if (p->k1_graph) cudaGraphDestroy(p->k1_graph);
     for (void* a : p->allocations) cudaFree(a);
@@ -585,6 +586,31 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
     pobk_status st = solve_finish(*plans[b], os[b], reps ? reps + b : nullptr);
     if (st != POBK_OK) return st;
   }
+  return POBK_OK;
+}
+
+pobk_status pobk_solve_multi(pobk_plan_t plan, int32_t R, const double* const* f, double* const* x,
+                             const double* const* xstar, const pobk_solve_opts* opts, void* stream, pobk_report* reps) {
+  g_err.clear();
+  if (R < 1 || R > kMaxRHS) return fail(POBK_ERR_ARG, "R must be in [1, " + std::to_string(kMaxRHS) + "]");
+  if (!f || !x || !reps) return fail(POBK_ERR_ARG, "f, x and reps must be non-NULL");
+  pobk_solve_opts o;
+  for (int32_t r = 0; r < R; r++) {
+    pobk_status st = check_solve_args(plan, f[r], x[r], xstar ? xstar[r] : nullptr, o, opts);
+    if (st != POBK_OK) {
+      g_err = "right-hand side " + std::to_string(r) + ": " + g_err;
+      return st;
+    }
+  }
+  if (o.stop == POBK_STOP_RELRES) return fail(POBK_ERR_ARG, "pobk_solve_multi supports POBK_STOP_RSE and POBK_STOP_NONE");
+  if (plan->any_overlap || plan->kernel == POBK_KERNEL_BLOCKS)
+    return fail(POBK_ERR_ARG, "pobk_solve_multi needs a row-level plan with thr = 0 (disjoint categories)");
+  for (int32_t r = 0; r < R; r++)
+    for (int32_t q = 0; q < r; q++)
+      if (x[q] == x[r]) return fail(POBK_ERR_ARG, "x pointers must be distinct");
+  DeviceGuard g(plan->device);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  CUDA_TRY(k1m_solve(*plan, R, f, x, xstar, o, (cudaStream_t)stream, reps));
   return POBK_OK;
 }
 

@@ -106,7 +106,8 @@ struct SliceLayout {
 struct SyncState {
   unsigned long long arrive;   // monotonic: T per completed sweep (64-bit: no wrap at any sweep count)
   unsigned long long arrive2;  // monotonic: T per RELRES publication (x~ of the shared columns)
-  long long pad0[14];
+  int die_next[2];             // tile placement by die (a.place): next tile from the low / high end
+  long long pad0[13];
 };
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -144,6 +145,8 @@ struct K2Args {
   int nap;                    // vector boundary slices: mailbox poll back-off (ns)
   int strict;                 // strict boundary priority (barrier 3 after every boundary post)
   int ireg;                   // register-resident interior slices (256-thread instantiation)
+  int place;                  // tile placement: 0 blockIdx, 1 by die (smid halves), 2 by die (smid parity)
+  int nsm;
 };
 
 // shared-memory control block
@@ -1017,7 +1020,23 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   int4* tmeta = cmeta + a.nck_max;                           // [ntask_max]
   double* xloc = (double*)(tmeta + a.ntask_max);             // [np_max + 1] private x~ + the zero slot
 
-  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ int s_tile;
+  if (threadIdx.x == 0) {
+    int tt = blockIdx.x;
+    if (a.place) {
+      // tile placement by die: tiles are numbered along the RCM slabs, so filling one die from
+      // tile 0 upwards and the other from tile T-1 downwards leaves one slab boundary between the
+      // dies (a cross-die mailbox hand-off is ~1.7x a same-die one)
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int die = a.place == 1 ? (smid >= (unsigned)a.nsm / 2u ? 1 : 0) : (int)(smid & 1u);
+      const int r = atomicAdd(&a.sync->die_next[die], 1);
+      tt = die == 0 ? r : a.T - 1 - r;
+    }
+    s_tile = tt;
+  }
+  __syncthreads();
+  const int t = s_tile, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s0 = a.tile_slice[t], nsl = a.tile_slice[t + 1] - s0;
   const int c0 = a.tile_chunk[t], nck = a.tile_chunk[t + 1] - c0;
   const int j0 = a.tile_task[t], ntask = a.tile_task[t + 1] - j0;
@@ -1411,6 +1430,7 @@ __global__ void k2_gather_xs(int n, const int* __restrict__ pmap, int nl, const 
 __global__ void k2_reset(SyncState* sync) {
   sync->arrive = 0;
   sync->arrive2 = 0;
+  sync->die_next[0] = sync->die_next[1] = 0;
 }
 
 // every mailbox slot empty, then each shared column's first reader of sweep 0 gets x~0
@@ -2153,6 +2173,12 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.trace_sweep = -1;
   a.nap = getenv("POBK_K2_NAP") ? atoi(getenv("POBK_K2_NAP")) : 0;  // (development knobs)
   a.strict = getenv("POBK_K2_STRICT") ? atoi(getenv("POBK_K2_STRICT")) : 0;
+  a.place = getenv("POBK_K2_PLACE") ? atoi(getenv("POBK_K2_PLACE")) : 0;
+  {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) a.nsm = v;
+    else a.nsm = 148;
+  }
   a.ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 1;
   static const char* trace_env = getenv("POBK_K2_TRACE");
   if (trace_env) {

@@ -23,6 +23,8 @@ struct DevCSR {
 struct K2Plan;  // cuda/k2_wavefront.cu
 struct K4Plan;  // cuda/k4_cluster.cu
 struct K5Plan;  // cuda/k5_blocks.cu
+struct MultiPlan;  // cuda/k1_multi.cu
+constexpr int kMaxRHS = 8;  // right-hand sides per pobk_solve_multi call
 
 struct Plan {
   int device = -1;
@@ -67,6 +69,7 @@ struct Plan {
   int pending_used = 0;
   K4Plan* k4 = nullptr;
   K5Plan* k5 = nullptr;            // the paper-literal k-block variant (pobk_blocks_preprocess)
+  MultiPlan* multi = nullptr;      // several right-hand sides in one sweep loop (pobk_solve_multi)
   BlockLayout blocks_host;         // its layout on host-only plans (device = -1)
   size_t k3_smem = 0;
   int32_t* k3_step_ptr = nullptr;  // [nsteps+1] device copy of the schedule steps
@@ -110,6 +113,10 @@ bool k4_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t
 cudaError_t k4_solve(Plan& p, cudaStream_t s, long long& launches);
 void k4_free(Plan& p);
 int k4_cluster_size(const Plan& p);
+// cuda/k1_multi.cu (R right-hand sides, A read once per step for all of them)
+cudaError_t k1m_solve(Plan& p, int R, const double* const* f, double* const* x, const double* const* xstar,
+                      const pobk_solve_opts& o, cudaStream_t s, pobk_report* reps);
+void k1m_free(Plan& p);
 // cuda/k5_blocks.cu (the paper-literal k-block variant)
 bool k5_build(Plan& p, const HostCSR& At, BlockLayout&& L, std::vector<std::vector<double>>&& ginv, std::string& why);
 cudaError_t k5_solve(Plan& p, cudaStream_t s, long long& launches);

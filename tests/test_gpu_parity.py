@@ -517,3 +517,48 @@ def test_batch_duplicate_plan_and_bad_args(env):
                                        ctypes.cast(XS, ctypes.c_void_p), ctypes.byref(o), None, ctypes.cast(reps, ctypes.c_void_p)))
     torch.cuda.synchronize()
     assert not x0[0].any().item()
+
+
+# ---------------------------------------------------------------- several right-hand sides (NEXT-3)
+@pytest.mark.parametrize("name,n,R,tol", [("lap3d7_64", 24, 3, 0.1), ("lap2d5_32", None, 8, 1e-3),
+                                          ("geoknn_1m", 30000, 4, 0.1)])
+def test_multi_rhs_bitwise_equals_single(env, name, n, R, tol):
+    """pobk_solve_multi: R right-hand sides of one matrix (Ax = f) in one sweep loop
+    -- A read once per step for all of them -- each stopping on its own RSE rule: every right-hand
+    side's stop sweep and iterates are bitwise those of its own single solve (and so the oracle's)."""
+    pk, torch = env
+    systems = [gen.make(name, b, n=n) if n else gen.make(name, b) for b in range(R)]
+    assert all(np.array_equal(s.data, systems[0].data) for s in systems)  # one matrix, R right-hand sides
+    plan = pk.Plan.from_system(systems[0])
+    fs = [_dev(torch, s.f) for s in systems]
+    xss = [_dev(torch, s.x_star) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = plan.solve_multi(fs, xs, xss, tol=tol)
+    for s, f, xst, x, r in zip(systems, fs, xss, xs, reps):
+        x1 = _dev(torch, np.zeros(s.m))
+        r1 = plan.solve(f, x1, xst, tol=tol)
+        assert r.sweeps == r1.sweeps and r.termination == r1.termination, (r.as_dict(), r1.as_dict())
+        assert np.array_equal(x.cpu().numpy(), x1.cpu().numpy())
+    pre = O.preprocess(systems[0].m, systems[0].indptr, systems[0].indices, systems[0].data)
+    assert np.array_equal(xs[-1].cpu().numpy(), O.run_sweeps(pre, systems[-1].f, reps[-1].sweeps))
+
+
+def test_multi_rhs_contract(env):
+    pk, torch = env
+    s = gen.make("lap2d5_32")
+    plan = pk.Plan.from_system(s)
+    f = _dev(torch, s.f)
+    with pytest.raises(pk.PobkError):
+        plan.solve_multi([f] * 9, [_dev(torch, np.zeros(s.m)) for _ in range(9)], None, stop="none", max_sweeps=3)
+    with pytest.raises(pk.PobkError):
+        plan.solve_multi([f, f], [_dev(torch, np.zeros(s.m)) for _ in range(2)], None, stop="relres")
+    x = _dev(torch, np.zeros(s.m))
+    with pytest.raises(pk.PobkError):  # the same x twice
+        plan.solve_multi([f, f], [x, x], None, stop="none", max_sweeps=3)
+    thr_plan = pk.Plan.from_system(s, thr=0.12)
+    with pytest.raises(pk.PobkError):
+        thr_plan.solve_multi([f], [x], None, stop="none", max_sweeps=3)
+    # fixed count, resume numbering
+    xs = [_dev(torch, np.zeros(s.m)) for _ in range(2)]
+    reps = plan.solve_multi([f, f], xs, None, stop="none", max_sweeps=12, sweep_offset=5)
+    assert [r.sweeps for r in reps] == [7, 7] and [r.sweeps_total for r in reps] == [12, 12]
