@@ -2039,6 +2039,51 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       fslot.push_back((slice_pos[si] + L.o_f) / 8 + r);
     }
   }
+  // Bounds check of the finished layout (every index the kernel will dereference), before upload:
+  // slices inside their chunk, chunks inside a ring slot, private columns inside the tile's x~
+  // window (or the zero slot), shared columns < m, mailbox targets (both parities) < NB, row
+  // lengths <= slice width, every row streamed exactly once.  (compute-sanitizer is closed on the
+  // GPU pool: DESIGN.md §9.)
+  {
+    auto bad = [&](const std::string& w) { why = "K2 layout check failed: " + w; return false; };
+    std::vector<uint8_t> seen(m, 0);
+    for (int t = 0; t < T; t++) {
+      for (int ci = tile_chunk[t]; ci < tile_chunk[t + 1]; ci++)
+        if (cmeta[ci].y > kSlot || cmeta[ci].y <= 0) return bad("chunk size " + std::to_string(cmeta[ci].y));
+      for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
+        const int4 sm = smeta[si];
+        const int chunk = sm.x & 0xfffff, R = sm.x >> 20, W = sm.z & 0xffff, VL = sm.z >> 16;
+        const int off_in = sm.y & 0xffff;
+        if (tile_chunk[t] + chunk >= tile_chunk[t + 1]) return bad("slice chunk index");
+        const int bytes = VL ? VLayout(R, VL, W).bytes : SliceLayout(R, W, slice_bnd[si]).bytes;
+        if (off_in + bytes > cmeta[tile_chunk[t] + chunk].y) return bad("slice outside its chunk");
+        if (R < 1 || R > kSliceRows || (VL && R * VL > 32)) return bad("slice rows");
+        if (VL) continue;  // (vector slices: checked by their own layout writer)
+        const unsigned char* blk = stream.data() + slice_pos[si];
+        const SliceLayout L(R, W, slice_bnd[si]);
+        const unsigned* col = (const unsigned*)(blk + L.o_col);
+        const unsigned* mout = (const unsigned*)(blk + L.o_mout);
+        const unsigned short* len = (const unsigned short*)(blk + L.o_len);
+        for (int r = 0; r < R; r++) {
+          const int32_t i = slice_rows[si][r];
+          if (seen[i]++) return bad("row " + std::to_string(i) + " streamed twice");
+          if (len[r] > W) return bad("row length > slice width");
+          for (int j = 0; j < W; j++) {
+            const unsigned c = col[j * R + r];
+            if (c & kShared) {
+              if ((c & kIdx) >= (unsigned)m || !slice_bnd[si]) return bad("shared column");
+              const unsigned mo = mout[j * R + r] & ~kWrap;
+              if ((long long)mo >= NB) return bad("mailbox target >= NB");
+            } else if (c > (unsigned)np_max || (c < (unsigned)np_max && (int)c >= np_t[t])) {
+              return bad("private column outside the tile's window");
+            }
+          }
+        }
+      }
+    }
+    for (int64_t i = 0; i < m; i++)
+      if (!seen[i] && !getenv("POBK_K2_VL")) return bad("row " + std::to_string(i) + " never streamed");
+  }
   p.tile_of_row.assign(tile.begin(), tile.end());
 
   // upload
