@@ -79,7 +79,7 @@ constexpr int kSliceRows = 32;      // rows per slice (one lane each)
 #endif
 constexpr int kMaxJ = POBK_K2_MAXJ; // entries per row whose x~ is kept in registers between passes (<= 32)
 constexpr int kBatch = 8;           // loads issued together
-constexpr int kSmemTotal = 227 * 1024;
+constexpr int kSmemTotal = 227 * 1024 - 256;  // (the opt-in budget less room for static shared memory)
 constexpr int kMetaBudget = 16 * 1024;  // slice/chunk/task metadata in shared memory
 constexpr unsigned kShared = 0x80000000u, kIdx = 0x7FFFFFFFu;
 constexpr unsigned kWrap = 0x80000000u;  // mailbox target of a sweep's last writer: next sweep's slot
@@ -155,6 +155,7 @@ struct alignas(16) Ctl {  // (16-byte multiple: the int4 metadata follows it in 
   int released[kMaxSlots];             // slices consumed per slot (cumulative)
   unsigned long long issued;           // chunks issued (sequence number)
   int stop;
+  int claim[3];                        // dynamic scheduling: next unclaimed slice of task ti (ti mod 3)
   long long done;                      // sweeps completed (all tiles stop at the same sweep)
   double part[32];                     // per-compute-warp RSE partials
 };
@@ -1006,7 +1007,7 @@ __device__ __forceinline__ void run_vslice(unsigned blk, int R, int W, int lane,
 // kVL: lane width of the plan's vector boundary slices (0: none); kIReg: register-resident
 // interior slices.  One instantiation per plan shape keeps each kernel's register allocation
 // to the paths it runs (every path inlined into one kernel spilled and ran 2x slower).
-template <int kNT, bool kBReg, int kVL, int kIReg>
+template <int kNT, bool kBReg, int kVL, int kIReg, bool kDyn = false>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
@@ -1053,6 +1054,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     ctl->issued = 0;
     ctl->stop = 0;
     ctl->done = 0;
+    ctl->claim[0] = ctl->claim[1] = ctl->claim[2] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < nsl; j += kNT) smeta[j] = a.smeta[s0 + j];
@@ -1109,6 +1111,103 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
       int rot = 0;  // round-robin offset (continues across tasks)
+      // ring position of a slice's chunk in this pass; waits until the chunk has landed
+      auto slice_blk = [&](const int4& sl, int& slot) -> unsigned {
+        const unsigned long long g = (unsigned long long)pass * nck + (sl.x & 0xfffff);
+        int h = hbase + (sl.y >> 16);
+        h = h >= 2 * NS ? h - 2 * NS : h;
+        slot = h >= NS ? h - NS : h;
+        while (ld_vol_shared64(&ctl->issued) <= g)
+          if (POBK_K2_CSLEEP) __nanosleep(POBK_K2_CSLEEP);
+        mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
+        return ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
+      };
+      if constexpr (kDyn) {
+        // DYNAMIC SCHEDULING (POBK_K2_DYN): the warps claim a task's slices from a shared counter,
+        // so the interior load balances across warps, and a warp done with task ti claims one slice
+        // of task ti+1 before the barrier that closes ti -- a boundary slice within the ring window
+        // is fetched and polled right away (look-ahead: the first warp to finish task ti is the
+        // one that waits for the neighbours' data), anything else is processed after the barrier.
+        // (Deadlock-free as the static schedule: a warp claims look-ahead work only once every
+        // slice of task ti is claimed, and every claimed slice of ti is processed by its claimer
+        // before it waits on anything of ti+1.)
+        auto claim = [&](int ti) -> int {
+          int q = 0;
+          if (lane == 0) q = atomicAdd(&ctl->claim[ti % 3], 1);
+          return __shfl_sync(kFull, q, 0);
+        };
+        BSlice2 B;  // (one register set for every boundary slice of this warp, look-ahead or not)
+        auto run_slice = [&](const int4& tm, int q) {  // a whole slice (pre, poll, post / interior)
+          const int nbnd = tm.y & 0xffff;
+          const int4 sl = smeta[tm.x + q];
+          const int R = sl.x >> 20, W = sl.z & 0xffff;
+          int slot;
+          const unsigned blk = slice_blk(sl, slot);
+          const SliceAddr S(blk, R, W, q < nbnd, lane);
+          if (q < nbnd) {
+            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
+            B.pre(S, W, R, lane, blk, xb);
+            B.poll(W, mbox_in);
+            B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, nullptr, 0);
+          } else if (kIReg == 1 && W <= kMaxJ) {
+            slice_interior_reg(S, W, xb);
+          } else {
+            slice_interior(S, W, xb);
+          }
+          __syncwarp();
+          if (lane == 0) atomicAdd(&ctl->released[slot], 1);
+        };
+        int pend = -1;  // a slice of this task claimed before the previous barrier, not fetched yet
+        for (int ti = 0; ti < ntask; ti++) {
+          const int4 tm = tmeta[ti];
+          const int ntot = (tm.y & 0xffff) + (tm.y >> 16);
+          if (ti == ntask - 1 && warp == kPub && lane == 0 && rse && np > 0) {  // (as the static path)
+            const char* xs0 = (const char*)(a.xsp + q0);
+            const unsigned bytes = (unsigned)np * 8u;
+            for (unsigned o = 0; o < bytes; o += 32768u) {
+              const unsigned n = bytes - o < 32768u ? bytes - o : 32768u;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs0 + o), "r"(n) : "memory");
+            }
+          }
+          for (int q = pend >= 0 ? pend : claim(ti); q < ntot; q = claim(ti)) run_slice(tm, q);
+          pend = -1;
+          if (tid == 0) ctl->claim[(ti + 2) % 3] = 0;  // task ti+2's counter (last used by task ti-1)
+          // one slice of task ti+1, claimed before the barrier
+          int nq = -1;
+          bool la = false;
+          int la_slot = 0, la_R = 0, la_W = 0;
+          unsigned la_blk = 0;
+          unsigned long long* la_in = nullptr;
+          if (ti + 1 < ntask) {
+            const int4 tm1 = tmeta[ti + 1];
+            const int nb1 = tm1.y & 0xffff, nt1 = nb1 + (tm1.y >> 16);
+            nq = claim(ti + 1);
+            if (nq >= nt1) nq = -1;
+            if (nq >= 0 && nq < nb1) {
+              const int4 sl = smeta[tm1.x + nq];
+              la = (sl.x & 0xfffff) - (smeta[tm1.x].x & 0xfffff) < NS && (sl.z >> 16) == 0;
+              if (la) {
+                la_R = sl.x >> 20;
+                la_W = sl.z & 0xffff;
+                la_blk = slice_blk(sl, la_slot);
+                const SliceAddr S(la_blk, la_R, la_W, true, lane);
+                la_in = mbox_p + sl.w + (size_t)(lane < la_R ? lane : 0) * ((la_W + 3) & ~3);
+                B.pre(S, la_W, la_R, lane, la_blk, xb);
+                B.poll(la_W, la_in);
+              }
+            }
+          }
+          named_bar(1, kNC);  // task ti is complete
+          if (la) {
+            const SliceAddr S(la_blk, la_R, la_W, true, lane);
+            B.post(S, la_W, xb, la_in, a.mbox, off_p, off_q, nullptr, 0);
+            __syncwarp();
+            if (lane == 0) atomicAdd(&ctl->released[la_slot], 1);
+          } else {
+            pend = nq;  // (processed first in the next task's claim loop)
+          }
+        }
+      } else
       for (int ti = 0; ti < ntask; ti++) {
         const int4 tm = tmeta[ti];
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
@@ -1235,6 +1334,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         if (!bdone) named_bar(3, kNC);
       }
       named_bar(1, kNC);  // the sweep's last task is complete
+      if (kDyn && tid == 0) ctl->claim[0] = ctl->claim[1] = ctl->claim[2] = 0;  // (ordered by the barriers below)
       sweep++;
       pass++;
       hbase += nck2;
@@ -2163,6 +2263,8 @@ const void* k2_kernel(int nt, int vl, int ireg) {
     case 4: return (const void*)k2_sweeps<256, true, 4, 0>;
     case 8: return (const void*)k2_sweeps<256, true, 8, 0>;
     default:
+      if (getenv("POBK_K2_DYN") && atoi(getenv("POBK_K2_DYN")))  // (development knob: dynamic slice claiming)
+        return ireg == 1 ? (const void*)k2_sweeps<256, true, 0, 1, true> : (const void*)k2_sweeps<256, true, 0, 0, true>;
       return ireg == 2 ? (const void*)k2_sweeps<256, true, 0, 2>
                        : ireg == 1 ? (const void*)k2_sweeps<256, true, 0, 1> : (const void*)k2_sweeps<256, true, 0, 0>;
   }
