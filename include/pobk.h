@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define POBK_ABI_VERSION 2
+#define POBK_ABI_VERSION 3
 
 typedef struct pobk_plan_s* pobk_plan_t;
 typedef int32_t pobk_status;
@@ -97,7 +97,15 @@ typedef struct {
                            sweeps of this call are numbered from sweep_offset + 1, so checks fall
                            on the same sweep numbers (multiples of check_every) and the cap on the
                            same total as in one uninterrupted solve; >= 0 */
+  int32_t order;        /* POBK_ORDER_SCHEDULE (default): the paper's cyclic schedule (Alg 5 loop,
+                           P:236-243); POBK_ORDER_RESIDUAL: every sweep applies the steps by
+                           decreasing ||f~_K - A~_K x~||^2 / ||A~_K||_F^2 taken at the sweep start
+                           (ties: ascending step), the greedy largest-residual rule of GRBK/GRMK
+                            that POBK itself avoids; thr = 0 row-level plans,
+                           runs on the launch path (reading R-G) */
 } pobk_solve_opts;
+
+enum { POBK_ORDER_SCHEDULE = 0, POBK_ORDER_RESIDUAL = 1 };
 
 typedef struct {
   int64_t sweeps;        /* sweeps performed by this call */

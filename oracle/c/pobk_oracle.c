@@ -340,6 +340,17 @@ void orc_sweep(int64_t m, const int64_t* indptr, const int32_t* indices, const d
   }
 }
 
+/* Residual of every row, r_i = f_i - sum_p a_ip x_{col p} (ascending p, from 0.0): the residual
+ * ordering's per-row input (DESIGN.md §3 reading R-G). */
+void orc_row_residuals(int64_t m, const int64_t* indptr, const int32_t* indices, const double* val,
+                       const double* f, const double* x, double* r) {
+  for (int64_t i = 0; i < m; i++) {
+    double s = 0.0;
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; p++) s = s + val[p] * x[indices[p]];
+    r[i] = f[i] - s;
+  }
+}
+
 /* ------------------------------------------------------------------ O8: stopping values
  * RSE = ||x - x*||_2 / ||x*||_2; RELRES = ||f - A x||_2 / ||f||_2.
  * Plain ascending sums of squares. */

@@ -24,6 +24,8 @@ __all__ = [
     "first_fit", "first_fit_py", "schedule", "category_overlap",
     "Preprocessed", "preprocess", "sweep", "sweep_rows_py", "sweep_numpy",
     "rse", "relres", "residual_norm", "SolveResult", "solve", "run_sweeps", "block_step_pinv",
+    "row_residuals", "seq_sum", "two_level_sum", "step_scores", "residual_order", "sweep_ordered",
+    "run_sweeps_ordered", "solve_ordered", "CHUNK",
     "build_c",
 ]
 
@@ -67,6 +69,7 @@ def _lib():
             lib.orc_first_fit.argtypes = [I64, P, P, P, P, ctypes.c_double, P]
             lib.orc_category_overlap.argtypes = [I64, P, P, P, I64, P]
             lib.orc_sweep.argtypes = [I64, P, P, P, P, P, P, I64, P, P, P, P]
+            lib.orc_row_residuals.argtypes = [I64, P, P, P, P, P, P]
             lib.orc_rse.argtypes = [I64, P, P]
             lib.orc_rse.restype = ctypes.c_double
             lib.orc_relres.argtypes = [I64, P, P, P, P, P]
@@ -462,3 +465,92 @@ def run_sweeps(pre: Preprocessed, f, nsweeps: int, x0=None) -> np.ndarray:
     x_t = permute_vector(np.zeros(pre.m) if x0 is None else x0, pre.perm)
     sweep(pre, f_t, x_t, nsweeps)
     return unpermute_vector(x_t, pre.perm)
+
+
+# ------------------------------------------------------------------ NEXT-4: residual-ordered sweep
+# Reading R-G: not the paper's POBK rule (P:248 avoids
+# residual selection) but the greedy "largest residual block first" idea of GRBK / GRMK
+# (Alg 1): at the start of every sweep each schedule step (category) K gets the score
+#     rho_K = ||f~_K - A~_K x~||^2 / ||A~_K||_F^2          (residuals and norms at the sweep start)
+# and the sweep applies the steps in decreasing rho (ties: ascending step index), each as in O7.
+# The two sums of a step run over its rows in schedule order in a fixed two-level grouping:
+# chunks of CHUNK consecutive rows summed left to right, then the chunk sums left to right.
+CHUNK = 256
+
+
+def row_residuals(pre: Preprocessed, f_t, x_t) -> np.ndarray:
+    r = np.empty(pre.m)
+    _lib().orc_row_residuals(pre.m, _p(pre.indptr), _p(pre.indices), _p(pre.data), _p(np.ascontiguousarray(f_t)),
+                             _p(np.ascontiguousarray(x_t)), _p(r))
+    return r
+
+
+def seq_sum(v) -> float:
+    """Left-to-right sum from 0.0 (no pairwise summation)."""
+    s = 0.0
+    for a in np.asarray(v, dtype=np.float64).tolist():
+        s = s + a
+    return s
+
+
+def two_level_sum(v, chunk: int = CHUNK) -> float:
+    v = np.asarray(v, dtype=np.float64)
+    return seq_sum([seq_sum(v[a:a + chunk]) for a in range(0, v.size, chunk)])
+
+
+def step_scores(pre: Preprocessed, f_t, x_t) -> np.ndarray:
+    r = row_residuals(pre, f_t, x_t)
+    out = np.empty(pre.nsteps)
+    for k in range(pre.nsteps):
+        rows = pre.cat_rows[pre.cat_ptr[k]:pre.cat_ptr[k + 1]]
+        out[k] = two_level_sum(r[rows] * r[rows]) / two_level_sum(pre.nrm2[rows])
+    return out
+
+
+def residual_order(scores) -> np.ndarray:
+    """Steps by decreasing score, ties by ascending index (a stable sort of -score)."""
+    return np.argsort(-np.asarray(scores), kind="stable").astype(np.int32)
+
+
+def _apply_step(pre: Preprocessed, k: int, f_t, x_t, scratch):
+    ptr = np.ascontiguousarray(pre.cat_ptr[k:k + 2], dtype=np.int64)
+    ov = np.ascontiguousarray(pre.overlap[k:k + 1], dtype=np.uint8)
+    _lib().orc_sweep(pre.m, _p(pre.indptr), _p(pre.indices), _p(pre.data), _p(pre.nrm2), _p(f_t), _p(x_t), 1,
+                     _p(ptr), _p(pre.cat_rows), _p(ov), _p(scratch))
+
+
+def sweep_ordered(pre: Preprocessed, f_t, x_t, nsweeps: int = 1, orders=None) -> np.ndarray:
+    """nsweeps residual-ordered sweeps (in place, RCM frame); `orders` collects each sweep's order."""
+    scratch = np.empty(max(pre.m, 1))
+    for _ in range(nsweeps):
+        order = residual_order(step_scores(pre, f_t, x_t))
+        if orders is not None:
+            orders.append(order)
+        for k in order:
+            _apply_step(pre, int(k), f_t, x_t, scratch)
+    return x_t
+
+
+def run_sweeps_ordered(pre: Preprocessed, f, nsweeps: int, x0=None) -> np.ndarray:
+    f_t = permute_vector(f, pre.perm)
+    x_t = permute_vector(np.zeros(pre.m) if x0 is None else x0, pre.perm)
+    sweep_ordered(pre, f_t, x_t, nsweeps)
+    return unpermute_vector(x_t, pre.perm)
+
+
+def solve_ordered(pre: Preprocessed, f, x_star, tol: float, max_sweeps: int):
+    """Residual-ordered sweeps to RSE < tol; returns (x user frame, sweeps, term, value)."""
+    f_t = permute_vector(f, pre.perm)
+    xs_t = permute_vector(x_star, pre.perm)
+    x_t = np.zeros(pre.m)
+    term, v, s = TERM_MAX_SWEEPS, float("nan"), 0
+    for s in range(1, max_sweeps + 1):
+        sweep_ordered(pre, f_t, x_t, 1)
+        v = rse(x_t, xs_t)
+        if not np.isfinite(v):
+            term = TERM_NONFINITE
+            break
+        if v < tol:
+            term = TERM_CONVERGED
+            break
+    return unpermute_vector(x_t, pre.perm), s, term, v

@@ -39,7 +39,7 @@ def _stream(stream):
     return ctypes.c_void_p(int(stream))
 
 
-def _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset=0) -> L.SolveOpts:
+def _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset=0, order="schedule") -> L.SolveOpts:
     o = L.SolveOpts()
     L.lib.pobk_solve_opts_default(ctypes.byref(o))
     o.tol = float(tol)
@@ -47,6 +47,7 @@ def _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset=0) -> L.SolveOp
     o.stop = L.STOP[stop] if isinstance(stop, str) else int(stop)
     o.check_every = int(check_every)
     o.sweep_offset = int(sweep_offset)
+    o.order = L.ORDER[order] if isinstance(order, str) else int(order)
     return o
 
 
@@ -146,11 +147,11 @@ class Plan:
 
     # ------------------------------------------------------------ solves
     def solve(self, f, x, x_star=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse", check_every: int = 1,
-              stream=None, sweep_offset: int = 0) -> Report:
+              stream=None, sweep_offset: int = 0, order: str = "schedule") -> Report:
         """x (CUDA float64, user frame) is x0 on entry and the solution on exit; sweep_offset > 0
         resumes a solve whose x0 already had that many sweeps (same check numbering and total cap)."""
         rep = L.Report()
-        o = _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset)
+        o = _solve_opts(tol, max_sweeps, stop, check_every, sweep_offset, order)
         L.check(L.lib.pobk_solve(self._h, _dev_ptr(f, "f", self.m), _dev_ptr(x, "x", self.m),
                                  _dev_ptr(x_star, "x_star", self.m), ctypes.byref(o), _stream(stream), ctypes.byref(rep)))
         return rep

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libpobk.so")
 OK, ERR_ARG, ERR_BAD_CSR, ERR_ZERO_ROW, ERR_UNSTABLE_THR, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE = range(8)
 TERM_CONVERGED, TERM_MAX_SWEEPS, TERM_NONFINITE = 0, 1, 2
 STOP = {"rse": 0, "relres": 1, "none": 2}
+ORDER = {"schedule": 0, "residual": 1}
 KERNEL = {"auto": 0, "launch": 1, "wavefront": 2, "smem": 3, "cluster": 4, "blocks": 5}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 TERM_NAME = {TERM_CONVERGED: "converged", TERM_MAX_SWEEPS: "max_sweeps", TERM_NONFINITE: "nonfinite"}
@@ -29,7 +30,7 @@ class PreprocessOpts(ctypes.Structure):
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_sweeps", ctypes.c_int64), ("stop", ctypes.c_int32),
-                ("check_every", ctypes.c_int32), ("sweep_offset", ctypes.c_int64)]
+                ("check_every", ctypes.c_int32), ("sweep_offset", ctypes.c_int64), ("order", ctypes.c_int32)]
 
 
 class BlocksOpts(ctypes.Structure):

@@ -69,6 +69,8 @@ void destroy_plan(Plan* p) {
     if (p->multi) k1m_free(*p);
     if (p->k1_exec) cudaGraphExecDestroy(p->k1_exec);
     if (p->k1_graph) cudaGraphDestroy(p->k1_graph);
+    if (p->k1o_exec) cudaGraphExecDestroy(p->k1o_exec);
+    if (p->k1o_graph) cudaGraphDestroy(p->k1o_graph);
     for (void* a : p->allocations) cudaFree(a);
     if (p->h_ctrl) cudaFreeHost(p->h_ctrl);
     for (auto& e : p->ev)
@@ -166,13 +168,18 @@ pobk_status solve_device(Plan& p, const double* f, double* x, const double* xsta
   // plans with vector boundary slices (opt-in) take RELRES on the K1 graph loop.
   int used = p.kernel;
   if (used == POBK_KERNEL_WAVEFRONT && o.stop == POBK_STOP_RELRES && !k2_relres_ok(p)) used = POBK_KERNEL_LAUNCH;
+  const bool ordered = o.order == POBK_ORDER_RESIDUAL;
+  if (ordered) used = POBK_KERNEL_LAUNCH;
   if (o.max_sweeps - o.sweep_offset > 0) {
     switch (used) {
       case POBK_KERNEL_SMEM: CUDA_TRY(k3_solve(p, s, launches)); break;
       case POBK_KERNEL_WAVEFRONT: CUDA_TRY(k2_solve(p, f, s, launches)); break;
       case POBK_KERNEL_CLUSTER: CUDA_TRY(k4_solve(p, s, launches)); break;
       case POBK_KERNEL_BLOCKS: CUDA_TRY(k5_solve(p, s, launches)); break;
-      default: CUDA_TRY(k1_solve(p, s, launches)); break;
+      default:
+        if (ordered) CUDA_TRY(k1_solve_ordered(p, s, launches));
+        else CUDA_TRY(k1_solve(p, s, launches));
+        break;
     }
   }
   CUDA_TRY(cudaEventRecord(p.ev[2], s));
@@ -195,7 +202,7 @@ pobk_status solve_finish(Plan& p, const pobk_solve_opts& o, pobk_report* rep) {
   CUDA_TRY(cudaEventElapsedTime(&t_sw, p.ev[1], p.ev[2]));
   const Ctrl& c = *p.h_ctrl;
   const bool ran = o.max_sweeps - o.sweep_offset > 0;
-  if (used == POBK_KERNEL_LAUNCH && ran) launches += c.sweeps * p.k1_nodes_per_sweep;
+  if (used == POBK_KERNEL_LAUNCH && ran) launches += c.sweeps * (o.order == POBK_ORDER_RESIDUAL ? p.k1o_nodes_per_sweep : p.k1_nodes_per_sweep);
   if (used == POBK_KERNEL_BLOCKS && ran) launches += c.sweeps * k5_nodes_per_sweep(p);
   if (rep) {
     rep->sweeps = ran ? c.sweeps : 0;
@@ -224,6 +231,9 @@ pobk_status check_solve_args(pobk_plan_t plan, const void* f, const void* x, con
   if (o.check_every < 1) return fail(POBK_ERR_ARG, "opts.check_every must be >= 1");
   if (o.max_sweeps < 0) return fail(POBK_ERR_ARG, "opts.max_sweeps must be >= 0");
   if (o.sweep_offset < 0) return fail(POBK_ERR_ARG, "opts.sweep_offset must be >= 0");
+  if (o.order != POBK_ORDER_SCHEDULE && o.order != POBK_ORDER_RESIDUAL) return fail(POBK_ERR_ARG, "opts.order out of range");
+  if (o.order == POBK_ORDER_RESIDUAL && (plan->any_overlap || plan->kernel == POBK_KERNEL_BLOCKS))
+    return fail(POBK_ERR_ARG, "the residual order needs a row-level plan with thr = 0");
   if (!(o.tol >= 0.0)) return fail(POBK_ERR_ARG, "opts.tol must be >= 0");
   return POBK_OK;
 }
@@ -251,6 +261,7 @@ void pobk_solve_opts_default(pobk_solve_opts* o) {
   o->stop = POBK_STOP_RSE;
   o->check_every = 1;
   o->sweep_offset = 0;
+  o->order = POBK_ORDER_SCHEDULE;
 }
 
 int32_t pobk_abi_version(void) { return POBK_ABI_VERSION; }

@@ -63,6 +63,9 @@ struct Plan {
   cudaGraph_t k1_graph = nullptr;
   cudaGraphExec_t k1_exec = nullptr;
   long long k1_nodes_per_sweep = 0;
+  cudaGraph_t k1o_graph = nullptr;       // the residual-ordered sweep loop (opts.order)
+  cudaGraphExec_t k1o_exec = nullptr;
+  long long k1o_nodes_per_sweep = 0;
 
   K2Plan* k2 = nullptr;
   long long pending_launches = 0;  // solve_device -> solve_finish (batched solves)
@@ -102,6 +105,7 @@ cudaError_t residual_sumsq(const Plan& p, const double* fs, const double* xt, co
 
 // cuda/k1_launch.cu
 cudaError_t k1_solve(Plan& p, cudaStream_t s, long long& launches);
+cudaError_t k1_solve_ordered(Plan& p, cudaStream_t s, long long& launches);
 // cuda/k3_smem.cu
 bool k3_fits(const Plan& p, size_t& smem_bytes);
 cudaError_t k3e_build(Plan& p, const std::vector<int32_t>& rp, const std::vector<int32_t>& col,

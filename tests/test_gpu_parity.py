@@ -562,3 +562,24 @@ def test_multi_rhs_contract(env):
     xs = [_dev(torch, np.zeros(s.m)) for _ in range(2)]
     reps = plan.solve_multi([f, f], xs, None, stop="none", max_sweeps=12, sweep_offset=5)
     assert [r.sweeps for r in reps] == [7, 7] and [r.sweeps_total for r in reps] == [12, 12]
+
+
+# ---------------------------------------------------------------- residual-ordered sweep (NEXT-4)
+@pytest.mark.parametrize("name,n,tol", [("lap2d5_32", None, 1e-2), ("randband_20k", 3000, 1e-6), ("lap3d7_64", 16, 0.1),
+                                        ("geoknn_1m", 20000, 0.1)])
+def test_residual_order_parity(env, name, n, tol):
+    """opts.order = residual (reading R-G): the device scores every step with the
+    oracle's fixed two-level sums, so it takes the same order decisions -- iterates bitwise the
+    oracle's residual-ordered sweeps (O7 per step), stop sweep +-1."""
+    pk, torch = env
+    s = gen.make(name, n=n) if n else gen.make(name)
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    plan = pk.Plan.from_system(s)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), max_sweeps=7, stop="none", order="residual")
+    assert rep.sweeps == 7 and rep.kernel == 1
+    assert np.array_equal(x.cpu().numpy(), O.run_sweeps_ordered(pre, s.f, 7))
+    xo, sweeps, term, v = O.solve_ordered(pre, s.f, s.x_star, tol, 20000)
+    x = _dev(torch, np.zeros(s.m))
+    rep = plan.solve(_dev(torch, s.f), x, _dev(torch, s.x_star), tol=tol, max_sweeps=20000, order="residual")
+    assert rep.termination == term and abs(rep.sweeps - sweeps) <= 1, (rep.sweeps, sweeps)

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol(pk):
     for name in sorted(declared):
         assert hasattr(lib, name), name
     assert set(pk._lib.SIGNATURES) == declared
-    assert lib.pobk_abi_version() == 2
+    assert lib.pobk_abi_version() == 3
 
 
 def _compare(pk, m, indptr, indices, data, thr=0.0, reorder=1):

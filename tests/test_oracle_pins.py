@@ -513,3 +513,64 @@ def test_thr_positive_partition_pins():
     # rows 0,2 now conflict (0.0704 >= 0.05)
     assert pre.color.tolist() == [0, 0, 1]
     assert pre.color.tolist() == O.first_fit_py(3, pre.indptr, pre.indices, pre.data, pre.nrm2, 0.05).tolist()
+
+
+# ------------------------------------------------------------------ NEXT-4 residual-ordered sweep (reading R-G)
+def test_residual_order_ties_and_permutation():
+    """Decreasing score, ties by ascending step index; always a permutation of the steps."""
+    assert O.residual_order([1.0, 3.0, 3.0, 2.0]).tolist() == [1, 2, 3, 0]
+    sc = np.random.default_rng(3).random(40)
+    assert sorted(O.residual_order(sc).tolist()) == list(range(40))
+
+
+def test_two_level_sum_grouping():
+    """Chunks summed left to right, then the chunk sums: 1 + 1e-16 + 1e-16 + 1e-16 in chunks of 2
+    is (1) + (2e-16) = 1 + 2^-52 (rounded up), while the plain left-to-right sum stays 1."""
+    v = [1.0, 1e-16, 1e-16, 1e-16]
+    assert O.seq_sum(v) == 1.0
+    assert O.two_level_sum(v, chunk=2) == 1.0 + 2.0 ** -52
+    assert O.two_level_sum([0.5, 0.25, 0.125, 1.0], chunk=2) == 1.875
+
+
+def test_step_scores_hand_value():
+    """rho_K = ||f_K - A_K x||^2 / ||A_K||_F^2: A = [[1,1],[1,-1]] (two one-row steps at thr = 0),
+    f = (3,-1), x = 0: rho = (9/2, 1/2) -> step 0 first; after x = (1.5, 1.5): rho = (0, 1/2)."""
+    A = sp.csr_matrix(np.array([[1.0, 1.0], [1.0, -1.0]]))
+    pre = _pre_from_matrix(A, reorder=0)
+    f = np.array([3.0, -1.0])
+    assert O.step_scores(pre, f, np.zeros(2)).tolist() == [4.5, 0.5]
+    assert O.step_scores(pre, f, np.array([1.5, 1.5])).tolist() == [0.0, 0.5]
+
+
+def test_ordered_steps_in_cyclic_order_equal_the_sweep():
+    """Applying the steps one at a time in schedule order is the O7 sweep, bitwise (the ordered
+    sweep differs only in the order)."""
+    s = gen.make("lap2d5_32")
+    pre = O.preprocess(s.m, s.indptr, s.indices, s.data)
+    f_t = O.permute_vector(s.f, pre.perm)
+    x1 = O.sweep(pre, f_t, np.zeros(s.m), 1)
+    x2 = np.zeros(s.m)
+    scratch = np.empty(s.m)
+    for k in range(pre.nsteps):
+        O.core._apply_step(pre, k, f_t, x2, scratch)
+    assert np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_ordered_sweep_monotone_and_converges(seed):
+    """Any order of exact projections keeps Eq 4.6 (error never increases) and the ordered
+    iteration reaches the dense solve."""
+    A = gen.scramble(gen.random_banded(40, 900 + seed, half=3), 950 + seed)
+    s = gen.from_csr("rb", A, seed)
+    pre = O.preprocess(40, s.indptr, s.indices, s.data)
+    f_t, xs_t = O.permute_vector(s.f, pre.perm), O.permute_vector(s.x_star, pre.perm)
+    x = np.zeros(40)
+    prev = np.linalg.norm(xs_t)
+    for _ in range(30):
+        O.sweep_ordered(pre, f_t, x, 1)
+        e = np.linalg.norm(x - xs_t)
+        assert e <= prev + 1e-12 * np.linalg.norm(xs_t)
+        prev = e
+    xo, sweeps, term, v = O.solve_ordered(pre, s.f, s.x_star, 1e-10, 100000)
+    assert term == O.TERM_CONVERGED
+    assert np.linalg.norm(xo - np.linalg.solve(A.toarray(), s.f)) <= 1e-8 * np.linalg.norm(s.x_star)
