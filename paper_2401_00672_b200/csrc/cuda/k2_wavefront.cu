@@ -191,6 +191,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "r"(parity)
       : "memory");
 }
+// POBK_K2_DEV (development builds only, default 0): the per-task trace stamps of one sweep
+// (POBK_K2_TRACE=<sweep>, tools/k2_trace.py and friends); production builds carry no trace code.
+#ifndef POBK_K2_DEV
+#if defined(POBK_K2_FT) || defined(POBK_K2_WT)
+#define POBK_K2_DEV 1
+#else
+#define POBK_K2_DEV 0
+#endif
+#endif
 // POBK_K2_FT (development): trace stamps in SM clock cycles instead of global nanoseconds, plus
 // stamps inside the boundary post (tools/k2_ft.py)
 #ifndef POBK_K2_FT
@@ -1109,7 +1118,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     while (sweep < maxs) {
       const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
-      const bool tr = a.trace != nullptr && sweep == a.trace_sweep;
+      const bool tr = POBK_K2_DEV && a.trace != nullptr && sweep == a.trace_sweep;
       int rot = 0;  // round-robin offset (continues across tasks)
       // ring position of a slice's chunk in this pass; waits until the chunk has landed
       auto slice_blk = [&](const int4& sl, int& slot) -> unsigned {
@@ -2327,7 +2336,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     else a.nsm = 148;
   }
   a.ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 1;
-  static const char* trace_env = getenv("POBK_K2_TRACE");
+  static const char* trace_env = POBK_K2_DEV ? getenv("POBK_K2_TRACE") : nullptr;  // (development builds)
   if (trace_env) {
     const size_t n = (size_t)k.T * k.ntask_max * 12;
     if (!k.trace) cudaMalloc(&k.trace, n * sizeof(unsigned long long));

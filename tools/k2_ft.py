@@ -1,4 +1,5 @@
-"""Cycle-level phases of K2's first boundary slice per task (development aid; needs a libpobk.so
+"""(Needs a development build: POBK_EXTRA_FLAGS=-DPOBK_K2_DEV=1, e.g. via tools/with_lib.sh.)
+Cycle-level phases of K2's first boundary slice per task (development aid; needs a libpobk.so
 built with -DPOBK_K2_FT=1): runs a traced solve and prints p10/p50/p90 cycles per phase.
 
     python tools/k2_ft.py [config] [sweep]

@@ -1,4 +1,5 @@
-"""In-situ mailbox hop latency of K2 (development aid).  Runs a traced solve (POBK_K2_TRACE), then
+"""(Needs a development build: POBK_EXTRA_FLAGS=-DPOBK_K2_DEV=1, e.g. via tools/with_lib.sh.)
+In-situ mailbox hop latency of K2 (development aid).  Runs a traced solve (POBK_K2_TRACE), then
 for every task's first boundary slice (q0) finds the producers of its shared inputs (previous
 toucher of each shared column in schedule order, wrapping to the previous sweep) and compares the
 consumer's poll-satisfied stamp with the latest producer's slice-done stamp.

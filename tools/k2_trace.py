@@ -1,4 +1,5 @@
-"""K2 per-task timeline of one sweep (development aid): POBK_K2_TRACE=<sweep> makes libpobk.so
+"""(Needs a development build: POBK_EXTRA_FLAGS=-DPOBK_K2_DEV=1, e.g. via tools/with_lib.sh.)
+K2 per-task timeline of one sweep (development aid): POBK_K2_TRACE=<sweep> makes libpobk.so
 dump %globaltimer stamps per tile and task; this script runs a solve and summarises where a
 sweep's time goes.  Stamps: 0 task start (warp 0), 1 boundary poll satisfied (warp 0), 3 task
 barrier passed, 4/5 first slice (q=0) ready/done, 6/7 first interior slice ready/done.

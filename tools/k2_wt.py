@@ -1,4 +1,5 @@
-"""Which warp closes each task barrier in K2 (development aid; libpobk.so built with
+"""(Needs a development build: POBK_EXTRA_FLAGS=-DPOBK_K2_DEV=1, e.g. via tools/with_lib.sh.)
+Which warp closes each task barrier in K2 (development aid; libpobk.so built with
 -DPOBK_K2_WT=1, 256 threads): per (tile, task) the compute warps' arrival clocks at the barrier
 that closes the task; reports how late the last warp is and whether it was a look-ahead warp
 (waiting for its poll = neighbours' data) or a warp still working on the task's slices.
