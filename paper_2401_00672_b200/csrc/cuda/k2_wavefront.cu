@@ -70,9 +70,16 @@ namespace {
 // Threads per CTA (one CTA per SM) is a template parameter of k2_sweeps: 256 (7 compute warps,
 // up to 255 registers: register-resident boundary slices, BSlice2) when a task has few slices,
 // 512 (15 compute warps, 128 registers: BSlice) when tasks have many (k2_build decides).
-constexpr int kSlot = 16 * 1024;    // ring slot (chunk) capacity, bytes
+#ifndef POBK_K2_SLOT_KB
+#define POBK_K2_SLOT_KB 24  // (measured r02: 16 KB 102.6 / 24 KB 98.1 / 32 KB 98.2 us per config-4 sweep; 32 KB
+                            //  starves the half-GPU config-5 tiles of private columns)
+#endif
+constexpr int kSlot = POBK_K2_SLOT_KB * 1024;  // ring slot (chunk) capacity, bytes
 static_assert(kSlot <= 65536, "slice offsets are packed in 16 bits");
-constexpr int kMinSlots = 4, kMaxSlots = 12;
+#ifndef POBK_K2_MAXSLOTS
+#define POBK_K2_MAXSLOTS 8
+#endif
+constexpr int kMinSlots = 4, kMaxSlots = POBK_K2_MAXSLOTS;
 constexpr int kSliceRows = 32;      // rows per slice (one lane each)
 #ifndef POBK_K2_MAXJ
 #define POBK_K2_MAXJ 24
