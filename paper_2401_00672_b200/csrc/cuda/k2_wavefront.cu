@@ -85,7 +85,16 @@ constexpr int kSliceRows = 32;      // rows per slice (one lane each)
 #define POBK_K2_MAXJ 24
 #endif
 constexpr int kMaxJ = POBK_K2_MAXJ; // entries per row whose x~ is kept in registers between passes (<= 32)
+static_assert(POBK_K2_MAXJ % 8 == 0 && POBK_K2_MAXJ <= 32, "the register window is processed in batches of 8");
 constexpr int kBatch = 8;           // loads issued together
+#ifndef POBK_K2_CHAIN
+#define POBK_K2_CHAIN 8
+#endif
+constexpr int kChainB = POBK_K2_CHAIN;  // boundary row sum: products of a group first, then its adds
+#ifndef POBK_K2_IBATCH
+#define POBK_K2_IBATCH 4  // (measured r02: 4 vs 8 -- config 4 97.6 vs 98.1 us/sweep, config 5 200.6 vs 190.3 G)
+#endif
+constexpr int kIB = POBK_K2_IBATCH;    // interior slices: entries per batch
 constexpr int kSmemTotal = 227 * 1024 - 256;  // (the opt-in budget less room for static shared memory)
 constexpr int kMetaBudget = 16 * 1024;  // slice/chunk/task metadata in shared memory
 constexpr unsigned kShared = 0x80000000u, kIdx = 0x7FFFFFFFu;
@@ -349,45 +358,45 @@ struct SliceAddr {
 // memory (unchanged in between: no other row of the category touches these columns)
 __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsigned xb) {
   double s = 0.0, n2 = 0.0;
-  for (int jb = 0; jb < W; jb += kBatch) {
-    unsigned c[kBatch];
-    double av[kBatch], xv[kBatch];
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB], xv[kIB];
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+    for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    for (int u = 0; u < kIB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
     // entries past the slice width contribute +0 * +0 (bit-exact no-ops): no per-entry branches,
     // so the next batch's loads can issue under this batch's arithmetic; the batch's products
     // first, then the two chains (common.cuh pin())
-    double pp[kBatch], qq[kBatch];
+    double pp[kIB], qq[kIB];
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) {
+    for (int u = 0; u < kIB; u++) {
       const bool in = jb + u < W;
       const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
       pp[u] = pin(__dmul_rn(a, x));
       qq[u] = pin(__dmul_rn(a, a));
     }
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) {
+    for (int u = 0; u < kIB; u++) {
       s = __dadd_rn(s, pp[u]);
       n2 = __dadd_rn(n2, qq[u]);
     }
   }
   const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
-  for (int jb = 0; jb < W; jb += kBatch) {
-    unsigned c[kBatch];
-    double av[kBatch], xv[kBatch];
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB], xv[kIB];
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) {
+    for (int u = 0; u < kIB; u++) {
       c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
       av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
     }
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) xv[u] = lds64(xb + 8u * c[u]);
+    for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
-    for (int u = 0; u < kBatch; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
+    for (int u = 0; u < kIB; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
   }
 }
 
@@ -668,13 +677,13 @@ struct BSlice2 {
     }
     double s = 0.0;
 #pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // per batch: products first, then the chain
+    for (int jb = 0; jb < kMaxJ; jb += kChainB) {  // per group: products first, then the chain
       if (jb < W) {
-        double pp[kBatch];
+        double pp[kChainB];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) pp[u] = pin(__dmul_rn(av[jb + u], xr[jb + u]));
+        for (int u = 0; u < kChainB; u++) pp[u] = pin(__dmul_rn(av[jb + u], xr[jb + u]));
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) s = __dadd_rn(s, pp[u]);
+        for (int u = 0; u < kChainB; u++) s = __dadd_rn(s, pp[u]);
       }
     }
     for (int j = kMaxJ; j < W; j++) {  // long rows: entries past the register window
