@@ -351,7 +351,7 @@ def main():
                    "m": s0.m, "nnz": s0.nnz, "systems_per_gpu": len(systems), "tol_rse": tol, "stop": "rse",
                    "sweeps_per_solve": all_reps[0].sweeps, "kernel": all_reps[0].as_dict()["kernel"],
                    "batch_lanes": nlanes,
-                   "tiles": stats["ntiles"], "private_nnz_frac": round(stats["private_nnz_frac"], 4),
+                   "tiles": stats["ntiles"], "threads_per_cta": stats["threads"], "private_nnz_frac": round(stats["private_nnz_frac"], 4),
                    "nsteps": plans[0].nsteps, "bandwidth_rcm": plans[0].bw_after,
                    "preprocess_s": round(plans[0].preprocess_seconds, 3),
                    "l2": ("working set %.1f MB fits the 126 MB L2: L2-resident by design (no flush); the HBM "

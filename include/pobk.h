@@ -156,7 +156,7 @@ typedef struct {
   int32_t kernel;
   int32_t ntiles;
   int32_t nchunks;
-  int32_t reserved;
+  int32_t threads;   /* K2: threads per CTA of the sweep kernel (256 or 512), else 0 */
   double private_nnz_frac;
   double interior_row_frac;
   int64_t stream_bytes;

@@ -39,7 +39,7 @@ class BlocksOpts(ctypes.Structure):
 
 class LayoutStats(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("ntiles", ctypes.c_int32), ("nchunks", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("private_nnz_frac", ctypes.c_double),
+                ("threads", ctypes.c_int32), ("private_nnz_frac", ctypes.c_double),
                 ("interior_row_frac", ctypes.c_double), ("stream_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:

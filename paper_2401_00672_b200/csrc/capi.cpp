@@ -472,6 +472,7 @@ pobk_status pobk_plan_get_layout_stats(pobk_plan_t p, pobk_layout_stats* out) {
   if (k2_stats(*p, st)) {
     out->ntiles = st.T;
     out->nchunks = st.nchunks;
+    out->threads = st.threads;
     out->private_nnz_frac = st.private_frac;
     out->interior_row_frac = st.interior_frac;
     out->stream_bytes = st.stream_bytes;

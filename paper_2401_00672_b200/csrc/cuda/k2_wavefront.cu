@@ -331,6 +331,18 @@ __device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsign
                : "memory");
 }
 
+// four predicated shared-memory loads in one asm block (registers keep their value where the
+// predicate is off)
+__device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, double& v3, unsigned p0, unsigned p1,
+                                           unsigned p2, unsigned p3, unsigned a0, unsigned a1, unsigned a2, unsigned a3) {
+  asm volatile(
+      "{\n .reg .pred q0, q1, q2, q3;\n setp.ne.u32 q0, %4, 0;\n setp.ne.u32 q1, %5, 0;\n setp.ne.u32 q2, %6, 0;\n"
+      " setp.ne.u32 q3, %7, 0;\n @q0 ld.shared.f64 %0, [%8];\n @q1 ld.shared.f64 %1, [%9];\n"
+      " @q2 ld.shared.f64 %2, [%10];\n @q3 ld.shared.f64 %3, [%11];\n}"
+      : "+d"(v0), "+d"(v1), "+d"(v2), "+d"(v3)
+      : "r"(p0), "r"(p1), "r"(p2), "r"(p3), "r"(a0), "r"(a1), "r"(a2), "r"(a3));
+}
+
 // A slice in the ring (shared-window address blk): lane r < R holds row r.  Entries j >= len_r
 // of a row are ELL padding: value +0 and the private "zero slot" column (x~ = +0, never written),
 // so including them in the sums adds +0 * +0 = +0 and changes no bit (a row sum starting at +0
@@ -450,44 +462,39 @@ struct BSlice {
     for (int j4 = 0; j4 < kMaxJ; j4 += 4)
       if (j4 < W) stm4_if((shm >> j4) & 0xFu, mbox_in + j4, kSentinel);
   }
-  // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity
+  // mbox: the mailbox array; off_p / off_q: index offsets of this sweep's / the next sweep's parity.
+  // Entries are processed in groups of 4 (a 9-entry row -- config 5 -- touches 12 slots, not 16);
+  // ||a~||^2 comes from the stream (the host's row_sqnorms, the oracle's O1 order).
   __device__ __forceinline__ void post(const SliceAddr& S, int W, unsigned xb, unsigned long long* mbox_in,
                                        unsigned long long* mbox, unsigned off_p, unsigned off_q, int R,
                                        unsigned long long* trp) {
-    double s = 0.0, n2 = 0.0;
+    constexpr int kG = 4;
+    const double n2 = lds64(S.vb + (unsigned)SliceLayout(R, W, true).o_n2);  // (vb = block + 8 * lane)
+    double s = 0.0;
 #pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+    for (int jb = 0; jb < kMaxJ; jb += kG) {
       if (jb < W) {
-        // a batch: columns, then the private x~ (always a valid address: branch-free), then the
+        // a group: columns, then the private x~ (always a valid address: branch-free), then the
         // values -- all loads in flight before the first use
-        static_assert(kBatch == 8, "batched loads are written for 8");
-        double av[kBatch], xp[kBatch];
-        unsigned cr[kBatch], ad[kBatch];
+        double av[kG], xp[kG];
+        unsigned cr[kG];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = S.cb + min(jb + u, W - 1) * S.cs;
-        lds32x8(cr, ad);
+        for (int u = 0; u < kG; u++) cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+        lds64x4_if(xp[0], xp[1], xp[2], xp[3], 1u, 1u, 1u, 1u, xb + 8u * ((cr[0] & kShared) ? 0u : cr[0]),
+                   xb + 8u * ((cr[1] & kShared) ? 0u : cr[1]), xb + 8u * ((cr[2] & kShared) ? 0u : cr[2]),
+                   xb + 8u * ((cr[3] & kShared) ? 0u : cr[3]));
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = xb + 8u * ((cr[u] & kShared) ? 0u : cr[u]);
-        lds64x8(xp, ad);
+        for (int u = 0; u < kG; u++) av[u] = jb + u < W ? lds64(S.vb + min(jb + u, W - 1) * S.vs) : 0.0;
+        double pp[kG];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) ad[u] = S.vb + min(jb + u, W - 1) * S.vs;
-        lds64x8(av, ad);
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) av[u] = jb + u < W ? av[u] : 0.0;
-        double pp[kBatch], qq[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {  // past the width: +0 * +0 (xr, av are +0 there)
+        for (int u = 0; u < kG; u++) {  // past the width: +0 * +0 (xr, av are +0 there)
           const int j = jb + u;
           const bool priv = j < W && !(cr[u] & kShared);
           xr[j] = ((shm >> j) & 1u) ? xr[j] : (priv ? xp[u] : 0.0);
           pp[u] = pin(__dmul_rn(av[u], xr[jb + u]));
-          qq[u] = pin(__dmul_rn(av[u], av[u]));
         }
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) {
-          s = __dadd_rn(s, pp[u]);
-          n2 = __dadd_rn(n2, qq[u]);
-        }
+        for (int u = 0; u < kG; u++) s = __dadd_rn(s, pp[u]);
       }
     }
     for (int j = kMaxJ; j < W; j++) {
@@ -504,7 +511,6 @@ struct BSlice {
         x = lds64(xb + 8u * (cj & kIdx));
       }
       s = __dadd_rn(s, __dmul_rn(a, x));
-      n2 = __dadd_rn(n2, __dmul_rn(a, a));
     }
     if (trp) {
       double s2 = s;
@@ -520,32 +526,20 @@ struct BSlice {
       if ((threadIdx.x & 31) == 0) trp[9] = gtimer();
     }
 #pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // new x~ (in place)
+    for (int jb = 0; jb < kMaxJ; jb += kG) {  // new x~ (in place), then the write-back of the group
       if (jb < W) {
-        double av[kBatch];
+        double av[kG];
+        unsigned mo[kG], cr[kG];
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) xr[jb + u] = __dadd_rn(xr[jb + u], __dmul_rn(alpha, av[u]));
-      }
-    }
-    if (POBK_K2_FT && trp) {
-      double a2 = xr[0];
-      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
-      if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
-    }
-#pragma unroll
-    for (int jb = 0; jb < kMaxJ; jb += kBatch) {  // write back: a batch of mailbox targets, then its stores
-      if (jb < W) {
-        unsigned mo[kBatch], cr[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; u++) {
+        for (int u = 0; u < kG; u++) {
+          av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
           cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
           mo[u] = lds32(S.mb + min(jb + u, W - 1) * S.cs);
         }
 #pragma unroll
-        for (int u = 0; u < kBatch; u++) {
+        for (int u = 0; u < kG; u++) {
           const int j = jb + u;
+          xr[j] = __dadd_rn(xr[j], __dmul_rn(alpha, av[u]));
           const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
           sts64_if(act & (sh ^ 1u), xb + 8u * (cr[u] & kIdx), xr[j]);
           stm_if(act & sh, mbox + ((mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)),
@@ -572,18 +566,6 @@ struct BSlice {
     if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
-
-// four predicated shared-memory loads in one asm block (registers keep their value where the
-// predicate is off)
-__device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, double& v3, unsigned p0, unsigned p1,
-                                           unsigned p2, unsigned p3, unsigned a0, unsigned a1, unsigned a2, unsigned a3) {
-  asm volatile(
-      "{\n .reg .pred q0, q1, q2, q3;\n setp.ne.u32 q0, %4, 0;\n setp.ne.u32 q1, %5, 0;\n setp.ne.u32 q2, %6, 0;\n"
-      " setp.ne.u32 q3, %7, 0;\n @q0 ld.shared.f64 %0, [%8];\n @q1 ld.shared.f64 %1, [%9];\n"
-      " @q2 ld.shared.f64 %2, [%10];\n @q3 ld.shared.f64 %3, [%11];\n}"
-      : "+d"(v0), "+d"(v1), "+d"(v2), "+d"(v3)
-      : "r"(p0), "r"(p1), "r"(p2), "r"(p3), "r"(a0), "r"(a1), "r"(a2), "r"(a3));
-}
 
 // Register-resident boundary slice (the 256-thread instantiation): the row's values, one target
 // word per entry (a private entry's x~ address in shared memory, a shared entry's mailbox target)
@@ -2407,6 +2389,7 @@ bool k2_stats(const Plan& p, K2Stats& st) {
   st.interior_frac = p.k2->interior_frac;
   st.stream_bytes = p.k2->stream_bytes;
   st.nchunks = p.k2->nchunks;
+  st.threads = p.k2->nt;
   return true;
 }
 

@@ -130,7 +130,7 @@ void k5_free(Plan& p);
 // cuda/k2_wavefront.cu
 bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why);
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
-struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; };
+struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; int threads; };
 bool k2_stats(const Plan& p, K2Stats& st);
 bool k2_relres_ok(const Plan& p);
 void k2_free(Plan& p);
