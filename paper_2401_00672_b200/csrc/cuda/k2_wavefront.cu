@@ -90,7 +90,15 @@ constexpr int kBatch = 8;           // loads issued together
 #ifndef POBK_K2_CHAIN
 #define POBK_K2_CHAIN 8
 #endif
-constexpr int kChainB = POBK_K2_CHAIN;  // boundary row sum: products of a group first, then its adds
+constexpr int kChainB = POBK_K2_CHAIN;
+#ifndef POBK_K2_WB
+#define POBK_K2_WB 8
+#endif
+constexpr int kWB = POBK_K2_WB;
+#ifndef POBK_K2_RSEU
+#define POBK_K2_RSEU 4
+#endif
+constexpr int kRU = POBK_K2_RSEU;  // end-of-sweep RSE scan: loads in flight per thread  // boundary write-back: entries issued per group  // boundary row sum: products of a group first, then its adds
 #ifndef POBK_K2_IBATCH
 #define POBK_K2_IBATCH 4  // (measured r02: 4 vs 8 -- config 4 97.6 vs 98.1 us/sweep, config 5 200.6 vs 190.3 G)
 #endif
@@ -705,7 +713,7 @@ struct BSlice2 {
     }
 #pragma unroll
     for (int j = 0; j < kMaxJ; j++) {  // write back: the targets are in registers (pre)
-      if ((j & ~(kBatch - 1)) < W) {
+      if ((j & ~(kWB - 1)) < W) {
         const unsigned act = j < S.myl, sh = (shm >> j) & 1u;
         sts64_if(act & (sh ^ 1u), tg[j], xr[j]);
         stm_if(act & sh, mbox + ((tg[j] & ~kWrap) + ((tg[j] & kWrap) ? off_q : off_p)),
@@ -1420,12 +1428,12 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         const double2* xsp2 = (const double2*)(a.xsp + q0);  // (q0, np: multiples of 16)
         const int np2 = np >> 1;
         const double2* xl2 = (const double2*)xloc;
-        for (int j0 = tid; j0 < np2; j0 += 4 * kNC) {
-          double2 xs[4];
+        for (int j0 = tid; j0 < np2; j0 += kRU * kNC) {
+          double2 xs[kRU];
 #pragma unroll
-          for (int u = 0; u < 4; u++) xs[u] = j0 + u * kNC < np2 ? __ldg(xsp2 + j0 + u * kNC) : make_double2(0.0, 0.0);
+          for (int u = 0; u < kRU; u++) xs[u] = j0 + u * kNC < np2 ? __ldg(xsp2 + j0 + u * kNC) : make_double2(0.0, 0.0);
 #pragma unroll
-          for (int u = 0; u < 4; u++)
+          for (int u = 0; u < kRU; u++)
             if (j0 + u * kNC < np2) {
               const double2 xv = xl2[j0 + u * kNC];
               const double d0 = xv.x - xs[u].x, d1 = xv.y - xs[u].y;
@@ -1437,20 +1445,20 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         // two dependent global round trips per thread instead of two per element
         const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB;  // sweep = sweeps done
         const int lc1 = a.lastcol_ptr[t + 1];
-        for (int j0 = a.lastcol_ptr[t] + tid; j0 < lc1; j0 += 4 * kNC) {
-          int sl4[4];
-          double xs4[4];
+        for (int j0 = a.lastcol_ptr[t] + tid; j0 < lc1; j0 += kRU * kNC) {
+          int sl4[kRU];
+          double xs4[kRU];
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
+          for (int u = 0; u < kRU; u++) {
             const bool in = j0 + u * kNC < lc1;
             sl4[u] = in ? __ldg(a.lastslot + j0 + u * kNC) : 0;
             xs4[u] = in ? __ldg(a.lcx + j0 + u * kNC) : 0.0;
           }
-          unsigned long long w4[4];
+          unsigned long long w4[kRU];
 #pragma unroll
-          for (int u = 0; u < 4; u++) w4[u] = ldm_if(j0 + u * kNC < lc1 ? 1u : 0u, wrap + sl4[u], 0ull);
+          for (int u = 0; u < kRU; u++) w4[u] = ldm_if(j0 + u * kNC < lc1 ? 1u : 0u, wrap + sl4[u], 0ull);
 #pragma unroll
-          for (int u = 0; u < 4; u++)
+          for (int u = 0; u < kRU; u++)
             if (j0 + u * kNC < lc1) {
               const double d = __longlong_as_double((long long)w4[u]) - xs4[u];
               acc = fma(d, d, acc);
