@@ -30,9 +30,6 @@
 //    and streams 12 B per stored entry + 10 B (f~, length); a boundary row also streams its
 //    ||a~_i||^2 (8 B, the host's row_sqnorms in the same order) and 4 B per entry (the mailbox
 //    slot its new value goes to), all loaded before the task barrier.
-//  * Opt-in vector boundary slices (VSlice, POBK_K2_VL=4|8): L lanes per boundary row, row sum
-//    in the oracle's order through the slice's ring slot -- bitwise equal, measured slower on the
-//    BASELINE configs, kept as an option.
 //  * A task's boundary slices come first; their warps note the shared entries, poll the
 //    mailboxes, then read the private operands with the row sums; the interior slices run
 //    meanwhile on the other warps.
@@ -130,8 +127,7 @@ struct SliceLayout {
 struct SyncState {
   unsigned long long arrive;   // monotonic: T per completed sweep (64-bit: no wrap at any sweep count)
   unsigned long long arrive2;  // monotonic: T per RELRES publication (x~ of the shared columns)
-  int die_next[2];             // tile placement by die (a.place): next tile from the low / high end
-  long long pad0[13];
+  long long pad0[14];
 };
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -166,11 +162,6 @@ struct K2Args {
   int nsl_max, nck_max, ntask_max, np_max;  // shared-memory sizing
   unsigned long long* trace;  // optional [T*ntask_max*12] globaltimer stamps of one sweep (POBK_K2_TRACE=s)
   int trace_sweep;
-  int nap;                    // vector boundary slices: mailbox poll back-off (ns)
-  int strict;                 // strict boundary priority (barrier 3 after every boundary post)
-  int ireg;                   // register-resident interior slices (256-thread instantiation)
-  int place;                  // tile placement: 0 blockIdx, 1 by die (smid halves), 2 by die (smid parity)
-  int nsm;
 };
 
 // shared-memory control block
@@ -179,7 +170,6 @@ struct alignas(16) Ctl {  // (16-byte multiple: the int4 metadata follows it in 
   int released[kMaxSlots];             // slices consumed per slot (cumulative)
   unsigned long long issued;           // chunks issued (sequence number)
   int stop;
-  int claim[3];                        // dynamic scheduling: next unclaimed slice of task ti (ti mod 3)
   long long done;                      // sweeps completed (all tiles stop at the same sweep)
   double part[32];                     // per-compute-warp RSE partials
 };
@@ -737,292 +727,12 @@ struct BSlice2 {
     if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
-// Vector boundary slice ("lane-parallel boundary rows"): R rows x L lanes
-// (R*L = RL <= 32); entry j of row r sits at lane r*L + j%L of round q = j/L, so the x~ loads,
-// products, new values and write-back of one row are spread over L lanes (Q = ceil(W/L) rounds
-// each).  The row sum still runs in the oracle's order (common.cuh): each lane writes its products
-// back over its own values in the slice's ring slot, and every lane of the row's group reads the
-// row's products in entry order (16-byte pairs) and forms the same left-to-right chain, so the
-// group agrees on alpha with no broadcast -- bit for bit the one-lane result.  ||a~||^2 comes
-// from the stream (computed on the host in the same left-to-right order).  A lane's mailbox
-// slots are contiguous (round q at lane*Qp + q, Qp = Q rounded up to 4): one 256-bit poll load
-// per four rounds.
-//   stream block: val[Q*RL] (fp64) | f[R] | n2[R] (fp64) | col[Q*RL] (u32) | mout[Q*RL] (u32) | len[R] (u16)
-struct VLayout {
-  int Q, o_f, o_n2, o_col, o_mout, o_len, bytes;
-  __host__ __device__ VLayout(int R, int L, int W) {
-    Q = (W + L - 1) / L;
-    const int n = Q * R * L;
-    o_f = 8 * n;
-    o_n2 = o_f + 8 * R;
-    o_col = o_n2 + 8 * R;
-    o_mout = o_col + 4 * n;
-    o_len = o_mout + 4 * n;
-    bytes = a16(o_len + 2 * R);
-  }
-};
-__host__ __device__ constexpr int vslice_qmax(int L) { return L >= 8 ? 4 : 8; }  // rounds in registers: W <= qmax * L
-
-// predicated shared-memory access helpers for the vector slices (registers keep their value, or
-// nothing is stored, where the predicate is off; no branches)
-__device__ __forceinline__ void lds64_if(double& v, unsigned p, unsigned a) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.shared.f64 %0, [%2];\n}" : "+d"(v) : "r"(p), "r"(a));
-}
-__device__ __forceinline__ void lds128_if(double& x, double& y, unsigned p, unsigned a) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%3];\n}"
-               : "+d"(x), "+d"(y)
-               : "r"(p), "r"(a));
-}
-__device__ __forceinline__ unsigned lds32_if(unsigned p, unsigned a) {
-  unsigned v = 0u;
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q ld.shared.u32 %0, [%2];\n}" : "+r"(v) : "r"(p), "r"(a));
-  return v;
-}
-
-template <int L>
-struct VSlice {
-  static constexpr int kQ = vslice_qmax(L);
-  double xr[kQ], av[kQ];
-  unsigned tg[kQ];    // round q: private entry -> shared-window address of its x~; shared -> mailbox target
-  unsigned shm, prv;  // bit q: this lane's round-q entry is a real shared / a real private entry
-  double n2, f;
-  int Q, RL;
-  unsigned vq, pb;    // (live lanes) shared-window address of this lane's val entry 0; of its row's entry 0
-  // operands from the ring (before the barrier that closes the tile's previous task)
-  __device__ __forceinline__ void pre(unsigned blk, int R, int W, int lane, unsigned xb) {
-    RL = R * L;
-    const VLayout V(R, L, W);
-    Q = V.Q;
-    const bool live = lane < RL;
-    const int ln = live ? lane : 0, r = ln / L, l = ln - r * L;
-    vq = live ? blk + 8u * ln : 0u;
-    pb = blk + 8u * (r * L);
-    f = lds64(blk + (unsigned)V.o_f + 8u * r);
-    n2 = lds64(blk + (unsigned)V.o_n2 + 8u * r);
-    const int len = live ? (int)lds16(blk + (unsigned)V.o_len + 2u * r) : 0;
-    unsigned c[kQ], mo[kQ];
-#pragma unroll
-    for (int q = 0; q < kQ; q++) {
-      const unsigned in = q < Q ? 1u : 0u, e = (unsigned)((q < Q ? q : 0) * RL + ln);
-      c[q] = lds32_if(in, blk + (unsigned)V.o_col + 4u * e);
-      mo[q] = lds32_if(in, blk + (unsigned)V.o_mout + 4u * e);
-      av[q] = 0.0;
-      lds64_if(av[q], in & (live ? 1u : 0u), blk + 8u * e);  // (ELL padding: value +0)
-    }
-    shm = 0u;
-    prv = 0u;
-#pragma unroll
-    for (int q = 0; q < kQ; q++) {
-      const bool real = live && q < Q && q * L + l < len, sh = (c[q] & kShared) != 0u;
-      shm |= (real && sh) ? (1u << q) : 0u;
-      prv |= (real && !sh) ? (1u << q) : 0u;
-      tg[q] = sh ? mo[q] : xb + 8u * (c[q] & kIdx);
-      xr[q] = 0.0;
-    }
-  }
-  // this lane's slots: mbox_in[q], q < Q (contiguous, 32-byte aligned), polled until no sentinel
-  __device__ __forceinline__ void poll(unsigned long long* mbox_in, int nap) {
-    unsigned pend = shm;
-    double t[kQ];
-    for (int it = 0;; it++) {
-      if (it > 0 && nap > 0) __nanosleep(nap);  // back-off: spinning warps crowd the load/store unit
-#pragma unroll
-      for (int q4 = 0; q4 < kQ; q4 += 4) ldm4_if((pend >> q4) & 0xFu, mbox_in + q4, t[q4], t[q4 + 1], t[q4 + 2], t[q4 + 3]);
-      unsigned np = 0u;
-#pragma unroll
-      for (int q = 0; q < kQ; q++) {
-        const bool pq = (pend >> q) & 1u, empty = (unsigned long long)__double_as_longlong(t[q]) == kSentinel;
-        np |= (pq && empty) ? (1u << q) : 0u;
-        xr[q] = (pq && !empty) ? t[q] : xr[q];
-      }
-      pend = np;
-      if (!__any_sync(kFull, pend != 0u)) break;
-    }
-#pragma unroll
-    for (int q4 = 0; q4 < kQ; q4 += 4) stm4_if((shm >> q4) & 0xFu, mbox_in + q4, kSentinel);  // re-armed for the sweep after next
-  }
-  __device__ __forceinline__ void post(unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned long long* trp,
-                                       int prio) {
-    // private x~ (final once the tile's previous task is done), all in flight at once
-#pragma unroll
-    for (int q = 0; q < kQ; q++) lds64_if(xr[q], (prv >> q) & 1u, tg[q]);
-#if POBK_K2_PRIO
-    if (prio) {
-#pragma unroll
-      for (int q = 0; q < kQ; q++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[q]));
-      named_arrive(3, prio);
-    }
-#endif
-    if (POBK_K2_FT && trp) {  // all private x~ loads complete
-#pragma unroll
-      for (int q = 0; q < kQ; q++) asm volatile("mov.b64 %0, %0;" : "+d"(xr[q]));
-      if ((threadIdx.x & 31) == 0) trp[11] = gtimer();
-    }
-    // each lane's products over its own values in the ring slot (every lane read its values in
-    // pre), then the row's products in entry order, 16-byte pairs, loaded two rounds ahead of the
-    // left-to-right chain (padding products are +0: adding them is exact)
-#pragma unroll
-    for (int q = 0; q < kQ; q++) sts64_if(vq != 0u && q < Q, vq + 8u * (unsigned)(q * RL), __dmul_rn(av[q], xr[q]));
-    __syncwarp();
-    double pr[kQ][L];
-#pragma unroll
-    for (int q = 0; q < kQ; q++)
-#pragma unroll
-      for (int u = 0; u < L; u++) pr[q][u] = 0.0;
-    constexpr int kAhead = 2;
-#pragma unroll
-    for (int q = 0; q < kAhead && q < kQ; q++)
-#pragma unroll
-      for (int u = 0; u < L; u += 2) lds128_if(pr[q][u], pr[q][u + 1], q < Q, pb + 8u * (unsigned)(q * RL + u));
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < kQ; q++) {
-      if (q + kAhead < kQ) {
-#pragma unroll
-        for (int u = 0; u < L; u += 2)
-          lds128_if(pr[q + kAhead][u], pr[q + kAhead][u + 1], q + kAhead < Q, pb + 8u * (unsigned)((q + kAhead) * RL + u));
-      }
-      if (q < Q) {
-#pragma unroll
-        for (int u = 0; u < L; u++) s = __dadd_rn(s, pr[q][u]);
-      }
-    }
-    if (trp) {
-      double s2 = s;
-      asm volatile("mov.b64 %0, %0;" : "+d"(s2));
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
-    }
-    const double alpha = __ddiv_rn(__dsub_rn(f, s), n2);
-    if (trp) {
-      double a2 = alpha;
-      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) trp[9] = gtimer();
-    }
-#pragma unroll
-    for (int q = 0; q < kQ; q++) xr[q] = __dadd_rn(xr[q], __dmul_rn(alpha, av[q]));
-    if (POBK_K2_FT && trp) {
-      double a2 = xr[0];
-      asm volatile("mov.b64 %0, %0;" : "+d"(a2));
-      if ((threadIdx.x & 31) == 0) trp[6] = gtimer();
-    }
-#pragma unroll
-    for (int q = 0; q < kQ; q++) {
-      sts64_if((prv >> q) & 1u, tg[q], xr[q]);
-      stm_if((shm >> q) & 1u, mbox + ((tg[q] & ~kWrap) + ((tg[q] & kWrap) ? off_q : off_p)),
-             (unsigned long long)__double_as_longlong(xr[q]));
-    }
-    if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
-  }
-};
-
-// interior slice, register-resident x~ (256-thread instantiation, W <= kMaxJ): columns, then the
-// x~ they address, all in flight together and kept in registers; values are read once per pass.
-// Entries past the slice width are not read at all (slice_interior reads columns, values and x~
-// in both passes, padded to batches of 8).  Same operations in the same order (common.cuh).
-__device__ __forceinline__ void slice_interior_reg(const SliceAddr& S, int W, unsigned xb) {
-  unsigned c[kMaxJ];
-  double xv[kMaxJ];
-#pragma unroll
-  for (int j = 0; j < kMaxJ; j++) c[j] = lds32_if(j < W ? 1u : 0u, S.cb + (unsigned)j * S.cs);
-#pragma unroll
-  for (int j = 0; j < kMaxJ; j++) {
-    xv[j] = 0.0;
-    lds64_if(xv[j], j < W ? 1u : 0u, xb + 8u * c[j]);
-  }
-  double s = 0.0, n2 = 0.0;
-#pragma unroll
-  for (int jb = 0; jb < kMaxJ; jb += kBatch) {
-    if (jb < W) {  // entries past the width are +0 * +0: bit-exact no-ops
-      double av[kBatch], pp[kBatch], qq[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        av[u] = 0.0;
-        lds64_if(av[u], jb + u < W ? 1u : 0u, S.vb + (unsigned)(jb + u) * S.vs);
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        pp[u] = pin(__dmul_rn(av[u], xv[jb + u]));
-        qq[u] = pin(__dmul_rn(av[u], av[u]));
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        s = __dadd_rn(s, pp[u]);
-        n2 = __dadd_rn(n2, qq[u]);
-      }
-    }
-  }
-  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
-#pragma unroll
-  for (int jb = 0; jb < kMaxJ; jb += kBatch) {
-    if (jb < W) {
-      double av[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; u++) {
-        av[u] = 0.0;
-        lds64_if(av[u], jb + u < W ? 1u : 0u, S.vb + (unsigned)(jb + u) * S.vs);
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; u++)
-        sts64_if(jb + u < S.myl ? 1u : 0u, xb + 8u * c[jb + u], __dadd_rn(xv[jb + u], __dmul_rn(alpha, av[u])));
-    }
-  }
-}
-
-// interior slice, all operands register-resident (the kIReg = 2 instantiation, W <= kMaxJ):
-// columns and values, then the x~ they address -- two dependent shared-memory round trips per
-// slice in total -- and no second read in the update pass.  Same operations in the same order
-// (common.cuh).
-constexpr int kIJ = 20;  // register window of slice_interior_reg2 (config 4: rows of 15-28 entries, p99 22)
-__device__ __forceinline__ void slice_interior_reg2(const SliceAddr& S, int W, unsigned xb) {
-  unsigned c[kIJ];
-  double av[kIJ], xv[kIJ];
-#pragma unroll
-  for (int j = 0; j < kIJ; j++) {
-    const unsigned in = j < W ? 1u : 0u;
-    c[j] = lds32_if(in, S.cb + (unsigned)j * S.cs);
-    av[j] = 0.0;
-    lds64_if(av[j], in, S.vb + (unsigned)j * S.vs);
-  }
-#pragma unroll
-  for (int j = 0; j < kIJ; j++) {
-    xv[j] = 0.0;
-    lds64_if(xv[j], j < W ? 1u : 0u, xb + 8u * c[j]);
-  }
-  double s = 0.0, n2 = 0.0;
-#pragma unroll
-  for (int j = 0; j < kIJ; j++) {
-    if ((j & ~(kBatch - 1)) < W) {  // entries past the width are +0 * +0: bit-exact no-ops
-      s = __dadd_rn(s, __dmul_rn(av[j], xv[j]));
-      n2 = __dadd_rn(n2, __dmul_rn(av[j], av[j]));
-    }
-  }
-  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
-#pragma unroll
-  for (int j = 0; j < kIJ; j++)
-    sts64_if(j < S.myl ? 1u : 0u, xb + 8u * c[j], __dadd_rn(xv[j], __dmul_rn(alpha, av[j])));
-}
-
-// one vector boundary slice of lane width L: pre, poll, [barrier], post
-template <int L>
-__device__ __forceinline__ void run_vslice(unsigned blk, int R, int W, int lane, unsigned long long* mbox_s, bool bar,
-                                           int nc, unsigned xb, unsigned long long* mbox, unsigned off_p, unsigned off_q,
-                                           unsigned long long* trp, int prio, int nap) {
-  VSlice<L> V;
-  V.pre(blk, R, W, lane, xb);
-  if (trp && lane == 0) trp[8] = gtimer();
-  V.poll(mbox_s + (size_t)(lane < V.RL ? lane : 0) * ((V.Q + 3) & ~3), nap);
-  if (trp && lane == 0) trp[1] = gtimer();
-  if (bar) named_bar(1, nc);
-  if (trp && lane == 0) trp[3] = gtimer();
-  V.post(mbox, off_p, off_q, trp, prio);
-}
-
-// kVL: lane width of the plan's vector boundary slices (0: none); kIReg: register-resident
-// interior slices.  One instantiation per plan shape keeps each kernel's register allocation
-// to the paths it runs (every path inlined into one kernel spilled and ran 2x slower).
-template <int kNT, bool kBReg, int kVL, int kIReg, bool kDyn = false>
+// One instantiation per CTA shape: 256 threads (register-resident boundary slices, BSlice2) or
+// 512 threads (BSlice).  (Round-2 experiments -- vector boundary slices, register-resident
+// interior slices, dynamic slice claiming, strict boundary priority, tile placement by die --
+// were measured and removed; with every path inlined into one kernel ptxas
+// spilled and the sweep ran 2x slower.)
+template <int kNT, bool kBReg>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
@@ -1036,23 +746,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   int4* tmeta = cmeta + a.nck_max;                           // [ntask_max]
   double* xloc = (double*)(tmeta + a.ntask_max);             // [np_max + 1] private x~ + the zero slot
 
-  __shared__ int s_tile;
-  if (threadIdx.x == 0) {
-    int tt = blockIdx.x;
-    if (a.place) {
-      // tile placement by die: tiles are numbered along the RCM slabs, so filling one die from
-      // tile 0 upwards and the other from tile T-1 downwards leaves one slab boundary between the
-      // dies (a cross-die mailbox hand-off is ~1.7x a same-die one)
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      const int die = a.place == 1 ? (smid >= (unsigned)a.nsm / 2u ? 1 : 0) : (int)(smid & 1u);
-      const int r = atomicAdd(&a.sync->die_next[die], 1);
-      tt = die == 0 ? r : a.T - 1 - r;
-    }
-    s_tile = tt;
-  }
-  __syncthreads();
-  const int t = s_tile, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s0 = a.tile_slice[t], nsl = a.tile_slice[t + 1] - s0;
   const int c0 = a.tile_chunk[t], nck = a.tile_chunk[t + 1] - c0;
   const int j0 = a.tile_task[t], ntask = a.tile_task[t + 1] - j0;
@@ -1069,7 +763,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     ctl->issued = 0;
     ctl->stop = 0;
     ctl->done = 0;
-    ctl->claim[0] = ctl->claim[1] = ctl->claim[2] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < nsl; j += kNT) smeta[j] = a.smeta[s0 + j];
@@ -1126,103 +819,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = POBK_K2_DEV && a.trace != nullptr && sweep == a.trace_sweep;
       int rot = 0;  // round-robin offset (continues across tasks)
-      // ring position of a slice's chunk in this pass; waits until the chunk has landed
-      auto slice_blk = [&](const int4& sl, int& slot) -> unsigned {
-        const unsigned long long g = (unsigned long long)pass * nck + (sl.x & 0xfffff);
-        int h = hbase + (sl.y >> 16);
-        h = h >= 2 * NS ? h - 2 * NS : h;
-        slot = h >= NS ? h - NS : h;
-        while (ld_vol_shared64(&ctl->issued) <= g)
-          if (POBK_K2_CSLEEP) __nanosleep(POBK_K2_CSLEEP);
-        mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
-        return ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
-      };
-      if constexpr (kDyn) {
-        // DYNAMIC SCHEDULING (POBK_K2_DYN): the warps claim a task's slices from a shared counter,
-        // so the interior load balances across warps, and a warp done with task ti claims one slice
-        // of task ti+1 before the barrier that closes ti -- a boundary slice within the ring window
-        // is fetched and polled right away (look-ahead: the first warp to finish task ti is the
-        // one that waits for the neighbours' data), anything else is processed after the barrier.
-        // (Deadlock-free as the static schedule: a warp claims look-ahead work only once every
-        // slice of task ti is claimed, and every claimed slice of ti is processed by its claimer
-        // before it waits on anything of ti+1.)
-        auto claim = [&](int ti) -> int {
-          int q = 0;
-          if (lane == 0) q = atomicAdd(&ctl->claim[ti % 3], 1);
-          return __shfl_sync(kFull, q, 0);
-        };
-        BSlice2 B;  // (one register set for every boundary slice of this warp, look-ahead or not)
-        auto run_slice = [&](const int4& tm, int q) {  // a whole slice (pre, poll, post / interior)
-          const int nbnd = tm.y & 0xffff;
-          const int4 sl = smeta[tm.x + q];
-          const int R = sl.x >> 20, W = sl.z & 0xffff;
-          int slot;
-          const unsigned blk = slice_blk(sl, slot);
-          const SliceAddr S(blk, R, W, q < nbnd, lane);
-          if (q < nbnd) {
-            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
-            B.pre(S, W, R, lane, blk, xb);
-            B.poll(W, mbox_in);
-            B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, nullptr, 0);
-          } else if (kIReg == 1 && W <= kMaxJ) {
-            slice_interior_reg(S, W, xb);
-          } else {
-            slice_interior(S, W, xb);
-          }
-          __syncwarp();
-          if (lane == 0) atomicAdd(&ctl->released[slot], 1);
-        };
-        int pend = -1;  // a slice of this task claimed before the previous barrier, not fetched yet
-        for (int ti = 0; ti < ntask; ti++) {
-          const int4 tm = tmeta[ti];
-          const int ntot = (tm.y & 0xffff) + (tm.y >> 16);
-          if (ti == ntask - 1 && warp == kPub && lane == 0 && rse && np > 0) {  // (as the static path)
-            const char* xs0 = (const char*)(a.xsp + q0);
-            const unsigned bytes = (unsigned)np * 8u;
-            for (unsigned o = 0; o < bytes; o += 32768u) {
-              const unsigned n = bytes - o < 32768u ? bytes - o : 32768u;
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs0 + o), "r"(n) : "memory");
-            }
-          }
-          for (int q = pend >= 0 ? pend : claim(ti); q < ntot; q = claim(ti)) run_slice(tm, q);
-          pend = -1;
-          if (tid == 0) ctl->claim[(ti + 2) % 3] = 0;  // task ti+2's counter (last used by task ti-1)
-          // one slice of task ti+1, claimed before the barrier
-          int nq = -1;
-          bool la = false;
-          int la_slot = 0, la_R = 0, la_W = 0;
-          unsigned la_blk = 0;
-          unsigned long long* la_in = nullptr;
-          if (ti + 1 < ntask) {
-            const int4 tm1 = tmeta[ti + 1];
-            const int nb1 = tm1.y & 0xffff, nt1 = nb1 + (tm1.y >> 16);
-            nq = claim(ti + 1);
-            if (nq >= nt1) nq = -1;
-            if (nq >= 0 && nq < nb1) {
-              const int4 sl = smeta[tm1.x + nq];
-              la = (sl.x & 0xfffff) - (smeta[tm1.x].x & 0xfffff) < NS && (sl.z >> 16) == 0;
-              if (la) {
-                la_R = sl.x >> 20;
-                la_W = sl.z & 0xffff;
-                la_blk = slice_blk(sl, la_slot);
-                const SliceAddr S(la_blk, la_R, la_W, true, lane);
-                la_in = mbox_p + sl.w + (size_t)(lane < la_R ? lane : 0) * ((la_W + 3) & ~3);
-                B.pre(S, la_W, la_R, lane, la_blk, xb);
-                B.poll(la_W, la_in);
-              }
-            }
-          }
-          named_bar(1, kNC);  // task ti is complete
-          if (la) {
-            const SliceAddr S(la_blk, la_R, la_W, true, lane);
-            B.post(S, la_W, xb, la_in, a.mbox, off_p, off_q, nullptr, 0);
-            __syncwarp();
-            if (lane == 0) atomicAdd(&ctl->released[la_slot], 1);
-          } else {
-            pend = nq;  // (processed first in the next task's claim loop)
-          }
-        }
-      } else
       for (int ti = 0; ti < ntask; ti++) {
         const int4 tm = tmeta[ti];
         const int nbnd = tm.y & 0xffff, ntot = nbnd + (tm.y >> 16);
@@ -1266,20 +862,12 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
 #if POBK_K2_PRIO
         // boundary priority: the interior warps start the task once the look-ahead warps hold
         // their private operands (barrier 3: look-ahead warps arrive, the others sync)
-        if (kBReg && !la && !a.strict) named_bar(3, kNC);
+        if (kBReg && !la) named_bar(3, kNC);
 #endif
-        // strict boundary priority (a.strict): no interior slice of the task starts before every
-        // boundary slice of the task is posted (barrier 3, every compute warp once per task), so
-        // the boundary rows' shared-memory round trips do not queue behind the interior's traffic
-        bool bdone = !a.strict;
         for (int q = qs; q < qe; q += qstep) {
           const bool bnd = q < nbnd;
-          if (!bnd && !bdone) {
-            named_bar(3, kNC);
-            bdone = true;
-          }
           const int4 sl = smeta[tm.x + q];
-          const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z & 0xffff, VL = sl.z >> 16;
+          const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
           const unsigned long long g = (unsigned long long)pass * nck + chunk;
           // ring position of chunk g without 64-bit division: h = g mod 2NS from the sweep's base
           // and the chunk's residue (precomputed); slot = h mod NS, phase parity = h >= NS
@@ -1291,21 +879,6 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
           const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
-          if (kVL > 0 && bnd && VL) {  // vector boundary slice (L lanes per row)
-            unsigned long long* const mbox_s = mbox_p + sl.w;
-            const bool bar = la && q == qs && ti > 0;
-            const int prio = (kBReg && la && q == qs && !a.strict) ? kNC : 0;
-            unsigned long long* const vtr = (tr && q == 0) ? trp : nullptr;
-            if constexpr (kVL > 0) run_vslice<kVL>(blk, R, W, lane, mbox_s, bar, kNC, xb, a.mbox, off_p, off_q, vtr, prio, a.nap);
-            if (vtr) {
-              __syncwarp();
-              if (lane == 0) trp[10] = gtimer();
-            }
-            __syncwarp();
-            if (lane == 0) atomicAdd(&ctl->released[slot], 1);
-            if (tr && lane == 0 && q == 0) trp[5] = gtimer();
-            continue;
-          }
           const SliceAddr S(blk, R, W, bnd, lane);
           if (bnd) {
             unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
@@ -1320,7 +893,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (bar) named_bar(1, kNC);
               if (POBK_K2_WT && bar && wtp && lane == 0 && warp == 0) wtp[8] = clock64();
               if (tr && q == 0 && lane == 0) trp[3] = gtimer();
-              B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs && !a.strict) ? kNC : 0);
+              B.post(S, W, xb, mbox_in, a.mbox, off_p, off_q, (tr && q == 0) ? trp : nullptr, (la && q == qs) ? kNC : 0);
             } else {
               BSlice B;
               B.pre(S, W, xb);
@@ -1338,18 +911,14 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (lane == 0) trp[10] = gtimer();
             }
           } else {
-            if (kIReg == 2 && W <= kIJ) slice_interior_reg2(S, W, xb);
-            else if (kIReg == 1 && W <= kMaxJ) slice_interior_reg(S, W, xb);
-            else slice_interior(S, W, xb);
+            slice_interior(S, W, xb);
           }
           __syncwarp();
           if (lane == 0) atomicAdd(&ctl->released[slot], 1);
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 5 : 7] = gtimer();
         }
-        if (!bdone) named_bar(3, kNC);
       }
       named_bar(1, kNC);  // the sweep's last task is complete
-      if (kDyn && tid == 0) ctl->claim[0] = ctl->claim[1] = ctl->claim[2] = 0;  // (ordered by the barriers below)
       sweep++;
       pass++;
       hbase += nck2;
@@ -1387,7 +956,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           for (int q = 0; q < ntot; q++, rr = rr + 1 == kNCW ? 0 : rr + 1) {
             if (rr != warp) continue;
             const int4 sl = smeta[tm.x + q];
-            const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z & 0xffff;
+            const int chunk = sl.x & 0xfffff, R = sl.x >> 20, W = sl.z;
             const unsigned long long g = (unsigned long long)pass * nck + chunk;
             int h = hbase + (sl.y >> 16);
             h = h >= 2 * NS ? h - 2 * NS : h;
@@ -1396,7 +965,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (POBK_K2_CSLEEP) __nanosleep(POBK_K2_CSLEEP);
             mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
             const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
-            const SliceAddr S(blk, R, W, q < nbnd, lane);  // (one-lane layout: K2 keeps RELRES off VSlice plans)
+            const SliceAddr S(blk, R, W, q < nbnd, lane);
             if (lane < R) {
               double sr = 0.0;
               for (int j = 0; j < W; j++) {
@@ -1545,7 +1114,6 @@ __global__ void k2_gather_xs(int n, const int* __restrict__ pmap, int nl, const 
 __global__ void k2_reset(SyncState* sync) {
   sync->arrive = 0;
   sync->arrive2 = 0;
-  sync->die_next[0] = sync->die_next[1] = 0;
 }
 
 // every mailbox slot empty, then each shared column's first reader of sweep 0 gets x~0
@@ -1573,7 +1141,6 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 struct K2Plan {
   int T = 0, NS = 0;
   int nt = 256;                // threads per CTA: 256 (BSlice2) or 512 (BSlice), see k2_build
-  int vl = 0;                  // lane width of the vector boundary slices (0: one lane per row)
   size_t smem = 0;
   int nsl_max = 1, nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
@@ -1818,30 +1385,6 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
     nt_choice = (double)ns / std::max<long long>(ntk, 1) > 10.0 ? 512 : 256;
     if (const char* e = getenv("POBK_K2_THREADS")) nt_choice = atoi(e) == 512 ? 512 : 256;  // development override
   }
-  // boundary rows as vector slices of L lanes per row, one width per plan (0: one lane per row):
-  // 8 when the median task's boundary rows fit one 4-row slice per compute warp, else 4
-  int vl_plan = 0;
-  {
-    std::vector<int> nbr;
-    for (int t = 0; t < T; t++)
-      for (int k = 0; k < p.nsteps; k++) {
-        int nb = 0;
-        for (int32_t r : rows_tk[t][k]) nb += boundary[r];
-        if (nb) nbr.push_back(nb);
-      }
-    if (!nbr.empty() && getenv("POBK_K2_VL")) {  // (opt-in: slower than one lane per row so far)
-      std::nth_element(nbr.begin(), nbr.begin() + nbr.size() / 2, nbr.end());
-      const int nwc = nt_choice / 32 - 1, med = nbr[nbr.size() / 2];
-      vl_plan = (nt_choice == 512 || med <= 4 * nwc) ? 8 : 4;
-    }
-    if (const char* e = getenv("POBK_K2_VL")) {  // development override: 0, 4 or 8
-      const int v = atoi(e);
-      vl_plan = v == 0 ? 0 : (v == 4 && nt_choice == 256) ? 4 : 8;
-    }
-  }
-  std::vector<int64_t> mb_base(m, -1);  // boundary rows: mailbox base of their slice
-  std::vector<int16_t> mb_L(m, 0), mb_r(m, 0);
-  std::vector<int32_t> mb_RL(m, 0);  // (vector slices: slots per lane, Qp)
   std::vector<int4> smeta, cmeta, tmeta;
   std::vector<int> tile_slice(T + 1, 0), tile_chunk(T + 1, 0), tile_task(T + 1, 0);
   std::vector<std::vector<int32_t>> slice_rows;  // global slice order
@@ -1867,15 +1410,9 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         size_t a = 0;
         while (a < g.size()) {
           const int W = rlen(g[a]);
-          // a vector slice of 32/VL rows, or (rows past the register rounds) a one-lane slice
-          const int VL = (bnd && vl_plan && W <= vslice_qmax(vl_plan) * vl_plan) ? vl_plan : 0;
           size_t b = a;
-          if (VL) {
-            b = std::min(g.size(), a + (size_t)(32 / VL));
-          } else {
-            while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
-          }
-          const int R = (int)(b - a), bytes = VL ? VLayout(R, VL, W).bytes : SliceLayout(R, W, bnd).bytes;
+          while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
+          const int R = (int)(b - a), bytes = SliceLayout(R, W, bnd).bytes;
           for (size_t r = a; r < b; r++) pad += W - rlen(g[r]);
           if (chunk_bytes + bytes > kSlot) {  // open a new chunk
             chunk_local++;
@@ -1884,26 +1421,14 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
           }
           if (chunk_local >= (1 << 20)) { why = "too many chunks in tile " + std::to_string(t); return false; }
           int mbase = 0;
-          if (bnd && VL) {  // round q of lane r*VL + l: slot mbase + (r*VL + l)*Qp + q
-            const int Qp = ((W + VL - 1) / VL + 3) & ~3;
-            const long long n = (long long)Qp * R * VL;
-            if (2 * (NB + n) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
-            mbase = (int)NB;
-            for (int r = 0; r < R; r++) {
-              mb_base[g[a + r]] = NB;
-              mb_L[g[a + r]] = (int16_t)VL;
-              mb_RL[g[a + r]] = Qp;
-              mb_r[g[a + r]] = (int16_t)r;
-            }
-            NB += n;
-          } else if (bnd) {
+          if (bnd) {
             const int Wp = (W + 3) & ~3;  // a lane's slots: contiguous, 32-byte aligned groups of 4
             if (2 * (NB + (long long)Wp * R) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
             mbase = (int)NB;
             for (int r = 0; r < R; r++) mb_of_row[g[a + r]] = NB + (long long)r * Wp;
             NB += (long long)Wp * R;
           }
-          smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W | (VL << 16), mbase));
+          smeta.push_back(make_int4(chunk_local | (R << 20), chunk_bytes, W, mbase));
           slice_rows.emplace_back(g.begin() + a, g.begin() + b);
           slice_pos.push_back(off);
           slice_bnd.push_back(bnd);
@@ -1953,21 +1478,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       // wavefront), so an access group is (slice, entry j, half)
       for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
         const auto& rows = slice_rows[si];
-        const int W = smeta[si].z & 0xffff, VL = smeta[si].z >> 16;
-        if (VL) {  // vector slice: round q is one warp access, lane r*VL + j%VL
-          const int Q = (W + VL - 1) / VL;
-          for (int q = 0; q < Q; q++, ng += 2)
-            for (size_t r = 0; r < rows.size(); r++)
-              for (int l = 0; l < VL; l++) {
-                const int32_t i = rows[r];
-                const int j = q * VL + l;
-                if (j < rlen(i)) {
-                  const int32_t cg = At.col[At.ptr[i] + j];
-                  if (!shared[cg]) groups_of[local[cg]].push_back(ng + ((int)r * VL + l >= 16 ? 1 : 0));
-                }
-              }
-          continue;
-        }
+        const int W = smeta[si].z;
         for (int j = 0; j < W; j++, ng += 2)
           for (size_t r = 0; r < rows.size(); r++) {
             const int32_t i = rows[r];
@@ -2063,7 +1574,6 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
     auto slot_of = [&](int64_t q) -> int64_t {  // mailbox slot of CSR entry q (its row is a boundary row)
       const int32_t i = row_of_entry[q];
       const int64_t j = q - At.ptr[i];
-      if (mb_L[i]) return mb_base[i] + ((int64_t)mb_r[i] * mb_L[i] + j % mb_L[i]) * mb_RL[i] + j / mb_L[i];
       return mb_of_row[i] + j;
     };
     std::vector<std::vector<std::pair<int, int>>> per(T);
@@ -2095,42 +1605,9 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
   fslot.reserve(m);
   for (size_t si = 0; si < slice_rows.size(); si++) {
     const auto& rows = slice_rows[si];
-    const int R = (int)rows.size(), W = smeta[si].z & 0xffff, VL = smeta[si].z >> 16;
+    const int R = (int)rows.size(), W = smeta[si].z;
     const bool bnd = slice_bnd[si];
     unsigned char* blk = stream.data() + slice_pos[si];
-    if (VL) {  // vector slice (VSlice): entry j of row r at round j/VL, lane r*VL + j%VL
-      const VLayout V(R, VL, W);
-      const int Q = (W + VL - 1) / VL, RL = R * VL;
-      double* val = (double*)blk;
-      double* fv = (double*)(blk + V.o_f);
-      double* n2v = (double*)(blk + V.o_n2);
-      unsigned* col = (unsigned*)(blk + V.o_col);
-      unsigned* mout = (unsigned*)(blk + V.o_mout);
-      unsigned short* len = (unsigned short*)(blk + V.o_len);
-      for (int r = 0; r < R; r++) {
-        const int32_t i = rows[r];
-        for (int j = 0; j < Q * VL; j++) {
-          const int e = (j / VL) * RL + r * VL + j % VL;
-          if (j < rlen(i)) {
-            const int64_t q = At.ptr[i] + j;
-            const int32_t cg = At.col[q];
-            col[e] = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
-            val[e] = At.val[q];
-            mout[e] = shared[cg] ? mout_of_entry[q] : 0u;
-          } else {
-            col[e] = (unsigned)np_max;  // ELL padding: zero slot, value +0 (never stored: len)
-            val[e] = 0.0;
-            mout[e] = 0u;
-          }
-        }
-        len[r] = (unsigned short)rlen(i);
-        fv[r] = 0.0;
-        n2v[r] = nrm2[i];  // ||a~_i||^2, left to right from 0 (row_sqnorms: the oracle's O1 order)
-        orig_q.push_back(p.perm[i]);
-        fslot.push_back((slice_pos[si] + V.o_f) / 8 + r);
-      }
-      continue;
-    }
     const SliceLayout L(R, W, bnd);
     double* val = (double*)blk;
     double* fv = (double*)(blk + L.o_f);
@@ -2167,13 +1644,12 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         if (cmeta[ci].y > kSlot || cmeta[ci].y <= 0) return bad("chunk size " + std::to_string(cmeta[ci].y));
       for (int si = tile_slice[t]; si < tile_slice[t + 1]; si++) {
         const int4 sm = smeta[si];
-        const int chunk = sm.x & 0xfffff, R = sm.x >> 20, W = sm.z & 0xffff, VL = sm.z >> 16;
+        const int chunk = sm.x & 0xfffff, R = sm.x >> 20, W = sm.z;
         const int off_in = sm.y & 0xffff;
         if (tile_chunk[t] + chunk >= tile_chunk[t + 1]) return bad("slice chunk index");
-        const int bytes = VL ? VLayout(R, VL, W).bytes : SliceLayout(R, W, slice_bnd[si]).bytes;
+        const int bytes = SliceLayout(R, W, slice_bnd[si]).bytes;
         if (off_in + bytes > cmeta[tile_chunk[t] + chunk].y) return bad("slice outside its chunk");
-        if (R < 1 || R > kSliceRows || (VL && R * VL > 32)) return bad("slice rows");
-        if (VL) continue;  // (vector slices: checked by their own layout writer)
+        if (R < 1 || R > kSliceRows) return bad("slice rows");
         const unsigned char* blk = stream.data() + slice_pos[si];
         const SliceLayout L(R, W, slice_bnd[si]);
         const unsigned* col = (const unsigned*)(blk + L.o_col);
@@ -2197,7 +1673,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       }
     }
     for (int64_t i = 0; i < m; i++)
-      if (!seen[i] && !getenv("POBK_K2_VL")) return bad("row " + std::to_string(i) + " never streamed");
+      if (!seen[i]) return bad("row " + std::to_string(i) + " never streamed");
   }
   p.tile_of_row.assign(tile.begin(), tile.end());
 
@@ -2210,7 +1686,6 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
   // (register-resident boundary slices, 256 threads); tasks of many slices (config 5: ~16) need
   // the 15 compute warps of the 512-thread instantiation (measured: 84.6 vs 70.5 us/sweep)
   k->nt = nt_choice;
-  k->vl = vl_plan;
   k->nsl_max = nsl_max;
   k->nck_max = nck_max;
   k->ntask_max = ntask_max;
@@ -2272,17 +1747,8 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
 
 namespace {
 // the sweep kernel for a plan shape: threads per CTA, vector-slice width, interior mode
-const void* k2_kernel(int nt, int vl, int ireg) {
-  if (nt == 512) return vl ? (const void*)k2_sweeps<512, false, 8, 0> : (const void*)k2_sweeps<512, false, 0, 0>;
-  switch (vl) {
-    case 4: return (const void*)k2_sweeps<256, true, 4, 0>;
-    case 8: return (const void*)k2_sweeps<256, true, 8, 0>;
-    default:
-      if (getenv("POBK_K2_DYN") && atoi(getenv("POBK_K2_DYN")))  // (development knob: dynamic slice claiming)
-        return ireg == 1 ? (const void*)k2_sweeps<256, true, 0, 1, true> : (const void*)k2_sweeps<256, true, 0, 0, true>;
-      return ireg == 2 ? (const void*)k2_sweeps<256, true, 0, 2>
-                       : ireg == 1 ? (const void*)k2_sweeps<256, true, 0, 1> : (const void*)k2_sweeps<256, true, 0, 0>;
-  }
+const void* k2_kernel(int nt) {
+  return nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<256, true>;
 }
 }  // namespace
 
@@ -2333,15 +1799,6 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.np_max = k.np_max;
   a.trace = nullptr;
   a.trace_sweep = -1;
-  a.nap = getenv("POBK_K2_NAP") ? atoi(getenv("POBK_K2_NAP")) : 0;  // (development knobs)
-  a.strict = getenv("POBK_K2_STRICT") ? atoi(getenv("POBK_K2_STRICT")) : 0;
-  a.place = getenv("POBK_K2_PLACE") ? atoi(getenv("POBK_K2_PLACE")) : 0;
-  {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) a.nsm = v;
-    else a.nsm = 148;
-  }
-  a.ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 1;
   static const char* trace_env = POBK_K2_DEV ? getenv("POBK_K2_TRACE") : nullptr;  // (development builds)
   if (trace_env) {
     const size_t n = (size_t)k.T * k.ntask_max * 12;
@@ -2351,8 +1808,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const int ireg = getenv("POBK_K2_IREG") ? atoi(getenv("POBK_K2_IREG")) : 0;  // (development knob)
-  const void* fn = k2_kernel(k.nt, k.vl, ireg);
+  const void* fn = k2_kernel(k.nt);
   if ((e = raise_smem_limit(fn)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
@@ -2388,7 +1844,7 @@ void k2_free(Plan& p) {
 }
 
 // RELRES runs inside K2 on one-lane layouts (the residual pass reads slices in that layout)
-bool k2_relres_ok(const Plan& p) { return p.k2 && p.k2->vl == 0; }
+bool k2_relres_ok(const Plan& p) { return p.k2 != nullptr; }
 
 bool k2_stats(const Plan& p, K2Stats& st) {
   if (!p.k2) return false;
