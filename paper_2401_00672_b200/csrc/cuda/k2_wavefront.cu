@@ -754,6 +754,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   const long long maxs = a.ctrl->max_sweeps;
   const int mode = a.ctrl->stop_mode, every = a.ctrl->check_every;
   const bool rse = mode == POBK_STOP_RSE;
+  // (constant during the solve: read once, not on the end-of-sweep decision path)
+  const long long offset = a.ctrl->offset;
+  const double tol = a.ctrl->tol, sden = sqrt(a.ctrl->den);
 
   if (tid == 0) {
     for (int i = 0; i < kMaxSlots; i++) {
@@ -925,7 +928,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       hbase = hbase >= 2 * NS ? hbase - 2 * NS : hbase;
       // ---- end of sweep: a grid barrier every sweep (it also orders the mailbox re-arms of this
       //      sweep before the writes of the next ones); the stop test when due
-      const bool due_check = ((sweep + a.ctrl->offset) % every) == 0 || sweep >= maxs;
+      const bool due_check = ((sweep + offset) % every) == 0 || sweep >= maxs;
       const bool due = mode != POBK_STOP_NONE && due_check;
       if (mode == POBK_STOP_RELRES && due_check) {
         // RELRES = ||f~ - A~ x~||_2 / ||f~||_2 at the end of the sweep (the fused
@@ -1060,13 +1063,20 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         double v = 0.0;
         if (due) {
           double tot = 0.0;  // fixed order: lane l sums tiles l, l+32, ..., then a fixed butterfly
-          for (int b0 = 0; b0 < a.T; b0 += 32)
+          {  // (loads first, then the adds in the same order; T <= 160 in one round trip)
+            double pv[5];
+#pragma unroll
+            for (int u = 0; u < 5; u++) pv[u] = u * 32 + lane < a.T ? ld_cg(a.partials + par * a.T + u * 32 + lane) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 5; u++) tot += pv[u];
+          }
+          for (int b0 = 160; b0 < a.T; b0 += 32)
             tot += b0 + lane < a.T ? ld_cg(a.partials + par * a.T + b0 + lane) : 0.0;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
-          v = sqrt(tot) / sqrt(a.ctrl->den);
+          v = sqrt(tot) / sden;
           if (!isfinite(v)) { st = 1; term = POBK_TERM_NONFINITE; }
-          else if (v < a.ctrl->tol) { st = 1; term = POBK_TERM_CONVERGED; }
+          else if (v < tol) { st = 1; term = POBK_TERM_CONVERGED; }
         }
         if (lane == 0) {
           if (st && t == 0) {  // (every tile holds the same values)
