@@ -64,6 +64,7 @@ void destroy_plan(Plan* p) {
   if (p->device >= 0) {
     DeviceGuard g(p->device);
     if (p->k2) k2_free(*p);
+    if (p->k2r) k2r_free(*p);
     if (p->k4) k4_free(*p);
     if (p->k5) k5_free(*p);
     if (p->multi) k1m_free(*p);
@@ -80,6 +81,7 @@ void destroy_plan(Plan* p) {
 }
 
 pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows) {
+  p.k2_tile_rows = tile_rows;
   DeviceGuard g(p.device);
   if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice(" + std::to_string(p.device) + ") failed");
   const int64_t m = p.m;
@@ -622,7 +624,30 @@ pobk_status pobk_solve_multi(pobk_plan_t plan, int32_t R, const double* const* f
       if (x[q] == x[r]) return fail(POBK_ERR_ARG, "x pointers must be distinct");
   DeviceGuard g(plan->device);
   if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
-  CUDA_TRY(k1m_solve(*plan, R, f, x, xstar, o, (cudaStream_t)stream, reps));
+  Plan& p = *plan;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool rse = o.stop == POBK_STOP_RSE;
+  // K2 plans: right-hand sides in pairs through the two-RHS K2 plan (A~ streamed once per sweep
+  // for both), an odd last one through the plan's own solve; others: K1M (all R in one loop)
+  static const bool force_k1m = getenv("POBK_MULTI_KERNEL") && !strcmp(getenv("POBK_MULTI_KERNEL"), "launch");  // (development)
+  if (p.k2 && p.kernel == POBK_KERNEL_WAVEFRONT && R >= 2 && !force_k1m) {
+    if (!p.k2r) {
+      std::string why;
+      if (!k2r_build(p, why)) return fail(POBK_ERR_CUDA, "two-RHS K2 plan: " + why);
+    }
+    for (int32_t r = 0; r + 1 < R; r += 2) {
+      const double* ff[2] = {f[r], f[r + 1]};
+      double* xx[2] = {x[r], x[r + 1]};
+      const double* xs[2] = {rse ? xstar[r] : nullptr, rse ? xstar[r + 1] : nullptr};
+      CUDA_TRY(k2r_solve(p, ff, xx, xs, o, s, reps + r));
+    }
+    if (R & 1) {
+      pobk_status st = solve_device(p, f[R - 1], x[R - 1], rse ? xstar[R - 1] : nullptr, o, s, reps + R - 1);
+      if (st != POBK_OK) return st;
+    }
+    return POBK_OK;
+  }
+  CUDA_TRY(k1m_solve(p, R, f, x, xstar, o, s, reps));
   return POBK_OK;
 }
 

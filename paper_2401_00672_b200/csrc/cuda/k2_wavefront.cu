@@ -109,14 +109,14 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15LL); }
 
-// slice block (bytes): val[W*R] f[R] (fp64) | [boundary slices] n2[R] (fp64: ||a~||^2)
+// slice block (bytes): val[W*R] f[R*nf] (fp64; nf right-hand sides, row-major) | [boundary slices] n2[R] (fp64: ||a~||^2)
 //                      | col[W*R] (u32: shared flag | index)
 //                      | [boundary slices] mout[W*R] (u32: wrap flag | mailbox index) | len[R] (u16)
 struct SliceLayout {
   int o_f, o_n2, o_col, o_mout, o_len, bytes;
-  __host__ __device__ SliceLayout(int R, int W, bool bnd) {
+  __host__ __device__ SliceLayout(int R, int W, bool bnd, int nf = 1) {
     o_f = 8 * W * R;
-    o_n2 = o_f + 8 * R;
+    o_n2 = o_f + 8 * R * nf;
     o_col = o_n2 + (bnd ? 8 * R : 0);
     o_mout = o_col + 4 * W * R;
     o_len = o_mout + (bnd ? 4 * W * R : 0);
@@ -156,8 +156,13 @@ struct K2Args {
   const double* xsp;          // [pmap size] x~* of the private columns in tile-local order (RSE stop)
   const double* lcx;          // [lastcol size] x~* of the owned shared columns (RSE stop)
   SyncState* sync;
-  double* partials;           // [2*T]
+  double* partials;           // [2*kR*T]
   Ctrl* ctrl;
+  // the second right-hand side of a two-RHS plan (kR = 2): its x~, x~* gathers and stop record
+  double* xg1;
+  const double* xsp1;
+  const double* lcx1;
+  Ctrl* ctrl1;
   int T, NS;
   int nsl_max, nck_max, ntask_max, np_max;  // shared-memory sizing
   unsigned long long* trace;  // optional [T*ntask_max*12] globaltimer stamps of one sweep (POBK_K2_TRACE=s)
@@ -171,7 +176,9 @@ struct alignas(16) Ctl {  // (16-byte multiple: the int4 metadata follows it in 
   unsigned long long issued;           // chunks issued (sequence number)
   int stop;
   long long done;                      // sweeps completed (all tiles stop at the same sweep)
-  double part[32];                     // per-compute-warp RSE partials
+  double part[64];                     // per-compute-warp RSE partials (right-hand side q at 32 q + warp)
+  unsigned actm;                       // bit q: right-hand side q still iterating (two-RHS plans)
+  int pad1[3];
 };
 static_assert(sizeof(Ctl) % 16 == 0, "int4 metadata follows Ctl in shared memory");
 
@@ -329,6 +336,24 @@ __device__ __forceinline__ void stm_if(unsigned p, unsigned long long* a, unsign
                : "memory");
 }
 
+// two consecutive fp64 (a column's two right-hand sides, 16-byte aligned)
+__device__ __forceinline__ double2 lds128(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128_if(unsigned p, unsigned a, double v0, double v1) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.shared.v2.f64 [%1], {%2, %3};\n}" ::"r"(p), "r"(a), "d"(v0),
+               "d"(v1)
+               : "memory");
+}
+// a mailbox slot of a two-RHS plan: two words, each single-copy atomic (the reader checks both)
+__device__ __forceinline__ void stm2_if(unsigned p, unsigned long long* a, double v0, double v1) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.relaxed.gpu.global.v2.b64 [%1], {%2, %3};\n}" ::"r"(p),
+               "l"(a), "l"((unsigned long long)__double_as_longlong(v0)), "l"((unsigned long long)__double_as_longlong(v1))
+               : "memory");
+}
+
 // four predicated shared-memory loads in one asm block (registers keep their value where the
 // predicate is off)
 __device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, double& v3, unsigned p0, unsigned p1,
@@ -350,16 +375,17 @@ struct SliceAddr {
   unsigned vb, cb, mb;  // this lane's val / col / mout entry 0; entry j at + j*R*8 / + j*R*4
   unsigned vs, cs;      // strides
   int myl;              // row length (0 for lanes >= R)
-  double f;             // f~_i
-  __device__ __forceinline__ SliceAddr(unsigned blk, int R, int W, bool bnd, int lane) {
+  double f, f1;         // f~_i (f1: the second right-hand side's, nf = 2)
+  __device__ __forceinline__ SliceAddr(unsigned blk, int R, int W, bool bnd, int lane, int nf = 1) {
     const int ln = lane < R ? lane : 0;
     vs = 8u * R;
     cs = 4u * R;
-    const SliceLayout L(R, W, bnd);
+    const SliceLayout L(R, W, bnd, nf);
     vb = opaque(blk + 8u * ln);
     cb = opaque(blk + (unsigned)L.o_col + 4u * ln);
     mb = blk + (unsigned)L.o_mout + 4u * ln;
-    f = lds64(blk + (unsigned)L.o_f + 8u * ln);
+    f = lds64(blk + (unsigned)L.o_f + 8u * nf * ln);
+    f1 = nf > 1 ? lds64(blk + (unsigned)L.o_f + 8u * nf * ln + 8u) : 0.0;
     myl = lane < R ? (int)lds16(blk + (unsigned)L.o_len + 2u * ln) : 0;
   }
 };
@@ -727,13 +753,212 @@ struct BSlice2 {
     if (POBK_K2_FT && trp && (threadIdx.x & 31) == 0) trp[7] = gtimer();
   }
 };
+// ------------------------------------------------------------------ two right-hand sides (kR = 2)
+// A two-RHS plan (pobk_solve_multi) streams A~ once per sweep for both:
+// x~ is pair-interleaved in shared memory (column c's two values in one 16-byte word pair), a
+// mailbox slot holds the pair, f~ the pair per row.  Each right-hand side runs the per-row
+// contract of common.cuh on its own (same operations, same order as its single solve), so its
+// iterates are bitwise those of its own solve; a right-hand side that has met its stop rule is
+// frozen (its new values are its old ones: act bit q clear) while the other one iterates.
+__device__ __forceinline__ void slice_interior2(const SliceAddr& S, int W, unsigned xb, unsigned act) {
+  double s0 = 0.0, s1 = 0.0, n2 = 0.0;
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB];
+    double2 xv[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) xv[u] = lds128(xb + 16u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    double p0[kIB], p1[kIB], qq[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const bool in = jb + u < W;
+      const double a = in ? av[u] : 0.0, x0 = in ? xv[u].x : 0.0, x1 = in ? xv[u].y : 0.0;
+      p0[u] = pin(__dmul_rn(a, x0));
+      p1[u] = pin(__dmul_rn(a, x1));
+      qq[u] = pin(__dmul_rn(a, a));
+    }
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      s0 = __dadd_rn(s0, p0[u]);
+      s1 = __dadd_rn(s1, p1[u]);
+      n2 = __dadd_rn(n2, qq[u]);
+    }
+  }
+  const double al0 = __ddiv_rn(__dsub_rn(S.f, s0), n2), al1 = __ddiv_rn(__dsub_rn(S.f1, s1), n2);
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB];
+    double2 xv[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+      av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    }
+#pragma unroll
+    for (int u = 0; u < kIB; u++) xv[u] = lds128(xb + 16u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const double y0 = (act & 1u) ? __dadd_rn(xv[u].x, __dmul_rn(al0, av[u])) : xv[u].x;
+      const double y1 = (act & 2u) ? __dadd_rn(xv[u].y, __dmul_rn(al1, av[u])) : xv[u].y;
+      sts128_if(jb + u < S.myl, xb + 16u * c[u], y0, y1);
+    }
+  }
+}
+
+// boundary slice of a two-RHS plan (BSlice's structure; a lane's mailbox words: entry j's pair at
+// mbox_in + 2j, so one 256-bit load polls two entries)
+struct BSliceR2 {
+  double xr[kMaxJ][2];
+  unsigned shm;
+  __device__ __forceinline__ void pre(const SliceAddr& S, int W) {
+    shm = 0u;
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kBatch) {
+      if (jb < W) {
+        unsigned cr[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+        for (int u = 0; u < kBatch; u++) {
+          const bool sh = (cr[u] & kShared) && jb + u < S.myl;
+          shm |= sh ? (1u << (jb + u)) : 0u;
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ void poll(int W, unsigned long long* mbox_in) {
+    unsigned pend = shm;
+    while (true) {
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j += 2)
+        if (j < W) ldm4_if((pend >> j) & 3u, mbox_in + 2 * j, xr[j][0], xr[j][1], xr[j + 1][0], xr[j + 1][1]);
+      unsigned np = 0u;
+#pragma unroll
+      for (int j = 0; j < kMaxJ; j++)
+        if ((pend >> j) & 1u)
+          np |= ((unsigned long long)__double_as_longlong(xr[j][0]) == kSentinel ||
+                 (unsigned long long)__double_as_longlong(xr[j][1]) == kSentinel)
+                    ? (1u << j)
+                    : 0u;
+      pend = np;
+      if (!__any_sync(kFull, pend != 0u)) break;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxJ; j += 2)
+      if (j < W) stm4_if((shm >> j) & 3u, mbox_in + 2 * j, kSentinel);
+  }
+  __device__ __forceinline__ void post(const SliceAddr& S, int W, int R, unsigned xb, unsigned long long* mbox_in,
+                                       unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned act) {
+    constexpr int kG = 4;
+    const double n2 = lds64(S.vb + (unsigned)SliceLayout(R, W, true, 2).o_n2);  // (vb = block + 8 * lane)
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kG) {
+      if (jb < W) {
+        double av[kG];
+        double2 xp[kG];
+        unsigned cr[kG];
+#pragma unroll
+        for (int u = 0; u < kG; u++) cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+        for (int u = 0; u < kG; u++) xp[u] = lds128(xb + 16u * ((cr[u] & kShared) ? 0u : cr[u]));
+#pragma unroll
+        for (int u = 0; u < kG; u++) av[u] = jb + u < W ? lds64(S.vb + min(jb + u, W - 1) * S.vs) : 0.0;
+        double p0[kG], p1[kG];
+#pragma unroll
+        for (int u = 0; u < kG; u++) {
+          const int j = jb + u;
+          const bool priv = j < W && !(cr[u] & kShared), sh = (shm >> j) & 1u;
+          xr[j][0] = sh ? xr[j][0] : (priv ? xp[u].x : 0.0);
+          xr[j][1] = sh ? xr[j][1] : (priv ? xp[u].y : 0.0);
+          p0[u] = pin(__dmul_rn(av[u], xr[j][0]));
+          p1[u] = pin(__dmul_rn(av[u], xr[j][1]));
+        }
+#pragma unroll
+        for (int u = 0; u < kG; u++) {
+          s0 = __dadd_rn(s0, p0[u]);
+          s1 = __dadd_rn(s1, p1[u]);
+        }
+      }
+    }
+    for (int j = kMaxJ; j < W; j++) {  // long rows: entries past the register window
+      const unsigned cj = lds32(S.cb + j * S.cs);
+      const double a = lds64(S.vb + j * S.vs);
+      double x0 = 0.0, x1 = 0.0;
+      if ((cj & kShared) && j < S.myl) {
+        unsigned long long w0, w1;
+        do {
+          w0 = ldm_if(1u, mbox_in + 2 * j, 0ull);
+          w1 = ldm_if(1u, mbox_in + 2 * j + 1, 0ull);
+        } while (w0 == kSentinel || w1 == kSentinel);
+        x0 = __longlong_as_double((long long)w0);
+        x1 = __longlong_as_double((long long)w1);
+      } else if (!(cj & kShared)) {
+        const double2 v = lds128(xb + 16u * (cj & kIdx));
+        x0 = v.x;
+        x1 = v.y;
+      }
+      s0 = __dadd_rn(s0, __dmul_rn(a, x0));
+      s1 = __dadd_rn(s1, __dmul_rn(a, x1));
+    }
+    const double al0 = __ddiv_rn(__dsub_rn(S.f, s0), n2), al1 = __ddiv_rn(__dsub_rn(S.f1, s1), n2);
+#pragma unroll
+    for (int jb = 0; jb < kMaxJ; jb += kG) {
+      if (jb < W) {
+        double av[kG];
+        unsigned mo[kG], cr[kG];
+#pragma unroll
+        for (int u = 0; u < kG; u++) {
+          av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+          cr[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+          mo[u] = lds32(S.mb + min(jb + u, W - 1) * S.cs);
+        }
+#pragma unroll
+        for (int u = 0; u < kG; u++) {
+          const int j = jb + u;
+          const double y0 = (act & 1u) ? __dadd_rn(xr[j][0], __dmul_rn(al0, av[u])) : xr[j][0];
+          const double y1 = (act & 2u) ? __dadd_rn(xr[j][1], __dmul_rn(al1, av[u])) : xr[j][1];
+          const unsigned on = j < S.myl, sh = (shm >> j) & 1u;
+          sts128_if(on & (sh ^ 1u), xb + 16u * (cr[u] & kIdx), y0, y1);
+          stm2_if(on & sh, mbox + (2u * (mo[u] & ~kWrap) + ((mo[u] & kWrap) ? off_q : off_p)), y0, y1);
+        }
+      }
+    }
+    for (int j = kMaxJ; j < W; j++) {  // tail: the slot still holds the consumed pair (re-armed now)
+      const unsigned cj = lds32(S.cb + j * S.cs), idx = cj & kIdx;
+      const double a = lds64(S.vb + j * S.vs);
+      if ((cj & kShared) && j < S.myl) {
+        const double x0 = __longlong_as_double((long long)ldm_if(1u, mbox_in + 2 * j, 0ull));
+        const double x1 = __longlong_as_double((long long)ldm_if(1u, mbox_in + 2 * j + 1, 0ull));
+        stm_if(1u, mbox_in + 2 * j, kSentinel);
+        stm_if(1u, mbox_in + 2 * j + 1, kSentinel);
+        const double y0 = (act & 1u) ? __dadd_rn(x0, __dmul_rn(al0, a)) : x0;
+        const double y1 = (act & 2u) ? __dadd_rn(x1, __dmul_rn(al1, a)) : x1;
+        const unsigned mo = lds32(S.mb + j * S.cs);
+        stm2_if(1u, mbox + (2u * (mo & ~kWrap) + ((mo & kWrap) ? off_q : off_p)), y0, y1);
+      } else if (!(cj & kShared) && j < S.myl) {
+        const unsigned ca = xb + 16u * idx;
+        const double2 v = lds128(ca);
+        const double y0 = (act & 1u) ? __dadd_rn(v.x, __dmul_rn(al0, a)) : v.x;
+        const double y1 = (act & 2u) ? __dadd_rn(v.y, __dmul_rn(al1, a)) : v.y;
+        sts128_if(1u, ca, y0, y1);
+      }
+    }
+  }
+};
+
 // One instantiation per CTA shape: 256 threads (register-resident boundary slices, BSlice2) or
 // 512 threads (BSlice).  (Round-2 experiments -- vector boundary slices, register-resident
 // interior slices, dynamic slice claiming, strict boundary priority, tile placement by die --
 // were measured and removed; with every path inlined into one kernel ptxas
 // spilled and the sweep ran 2x slower.)
-template <int kNT, bool kBReg>
+template <int kNT, bool kBReg, int kR>
 __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
+  static_assert(kR == 1 || (kR == 2 && !kBReg), "two-RHS plans use the BSliceR2 boundary path");
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
   constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
@@ -757,6 +982,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   // (constant during the solve: read once, not on the end-of-sweep decision path)
   const long long offset = a.ctrl->offset;
   const double tol = a.ctrl->tol, sden = sqrt(a.ctrl->den);
+  const double sden1 = kR > 1 && rse ? sqrt(a.ctrl1->den) : 0.0;
+  unsigned actm = kR > 1 ? 3u : 1u;  // right-hand sides still iterating
 
   if (tid == 0) {
     for (int i = 0; i < kMaxSlots; i++) {
@@ -766,15 +993,17 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     ctl->issued = 0;
     ctl->stop = 0;
     ctl->done = 0;
+    ctl->actm = actm;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < nsl; j += kNT) smeta[j] = a.smeta[s0 + j];
   for (int j = tid; j < nck; j += kNT) cmeta[j] = a.cmeta[c0 + j];
   for (int j = tid; j < ntask; j += kNT) tmeta[j] = a.tmeta[j0 + j];
-  if (tid == 0) xloc[a.np_max] = 0.0;  // the zero slot of the ELL padding (never written)
+  if (tid < kR) xloc[kR * a.np_max + tid] = 0.0;  // the zero slot of the ELL padding (never written)
   for (int j = tid; j < np; j += kNT) {
     const int gcol = a.pmap[q0 + j];  // -1: a hole of the bank-aware placement
-    xloc[j] = gcol >= 0 ? a.xg[gcol] : 0.0;
+    xloc[kR * j] = gcol >= 0 ? a.xg[gcol] : 0.0;
+    if (kR > 1) xloc[kR * j + 1] = gcol >= 0 ? a.xg1[gcol] : 0.0;
   }
   __syncthreads();
 
@@ -818,7 +1047,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     const int nck2 = nck % (2 * NS);
     int hbase = 0;  // (pass * nck) mod 2NS
     while (sweep < maxs) {
-      const unsigned off_p = (unsigned)((sweep & 1) * a.NB), off_q = (unsigned)(((sweep + 1) & 1) * a.NB);
+      const unsigned off_p = (unsigned)((sweep & 1) * a.NB * kR), off_q = (unsigned)(((sweep + 1) & 1) * a.NB * kR);
       unsigned long long* const mbox_p = a.mbox + off_p;  // this sweep's slots
       const bool tr = POBK_K2_DEV && a.trace != nullptr && sweep == a.trace_sweep;
       int rot = 0;  // round-robin offset (continues across tasks)
@@ -839,11 +1068,13 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         if (tr && qs == 0 && lane == 0) trp[0] = gtimer();
         if (ti == ntask - 1 && warp == kPub && lane == 0 && rse && np > 0) {
           // the end-of-sweep RSE scan reads this tile's x~* next: bring it into L2 now
-          const char* xs0 = (const char*)(a.xsp + q0);
           const unsigned bytes = (unsigned)np * 8u;  // multiple of 128 (np: multiple of 16)
-          for (unsigned o = 0; o < bytes; o += 32768u) {
-            const unsigned n = bytes - o < 32768u ? bytes - o : 32768u;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs0 + o), "r"(n) : "memory");
+          for (int q = 0; q < kR; q++) {
+            const char* xs0 = (const char*)((q == 0 ? a.xsp : a.xsp1) + q0);
+            for (unsigned o = 0; o < bytes; o += 32768u) {
+              const unsigned n = bytes - o < 32768u ? bytes - o : 32768u;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs0 + o), "r"(n) : "memory");
+            }
           }
         }
         // LOOK-AHEAD: this warp's first boundary slice of task ti (q = qs).  Its operands and the
@@ -882,11 +1113,17 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           mbar_wait(&ctl->full[slot], h >= NS ? 1u : 0u);
           const unsigned blk = ring_s + (unsigned)(slot * kSlot + (sl.y & 0xffff));
           if (tr && lane == 0 && (q == 0 || (!POBK_K2_FT && q == nbnd))) trp[q == 0 ? 4 : 6] = gtimer();
-          const SliceAddr S(blk, R, W, bnd, lane);
+          const SliceAddr S(blk, R, W, bnd, lane, kR);
           if (bnd) {
-            unsigned long long* const mbox_in = mbox_p + sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3);
+            unsigned long long* const mbox_in = mbox_p + (size_t)kR * (sl.w + (size_t)(lane < R ? lane : 0) * ((W + 3) & ~3));
             const bool bar = la && q == qs && ti > 0;  // look-ahead slice: barrier after the poll
-            if constexpr (kBReg) {
+            if constexpr (kR == 2) {
+              BSliceR2 B;
+              B.pre(S, W);
+              B.poll(W, mbox_in);
+              if (bar) named_bar(1, kNC);
+              B.post(S, W, R, xb, mbox_in, a.mbox, off_p, off_q, actm);
+            } else if constexpr (kBReg) {
               BSlice2 B;
               B.pre(S, W, R, lane, blk, xb);
               if (tr && q == 0 && lane == 0) trp[8] = gtimer();
@@ -913,6 +1150,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               __syncwarp();
               if (lane == 0) trp[10] = gtimer();
             }
+          } else if constexpr (kR == 2) {
+            slice_interior2(S, W, xb, actm);
           } else {
             slice_interior(S, W, xb);
           }
@@ -930,7 +1169,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       //      sweep before the writes of the next ones); the stop test when due
       const bool due_check = ((sweep + offset) % every) == 0 || sweep >= maxs;
       const bool due = mode != POBK_STOP_NONE && due_check;
-      if (mode == POBK_STOP_RELRES && due_check) {
+      if (kR == 1 && mode == POBK_STOP_RELRES && due_check) {  // (two-RHS plans: RSE / none only)
         // RELRES = ||f~ - A~ x~||_2 / ||f~||_2 at the end of the sweep (the fused
         // SpMV + norm of the north star): (1) the last-writer tile of every shared column
         // publishes the column's sweep-final value (its wrap slot) to x~ in global memory; (2) a
@@ -991,7 +1230,74 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);  // fixed lane order
         if (lane == 0) ctl->part[warp] = acc;
       }
-      if (mode == POBK_STOP_RSE && due) {
+      if (kR == 2 && mode == POBK_STOP_RSE && due) {
+        // the scan below for both right-hand sides (x~ pairs in shared memory and the mailboxes),
+        // each in the single scan's order (so each RSE is bitwise its single solve's)
+        double acc0 = 0.0, acc1 = 0.0;
+        const double2* xl2 = (const double2*)xloc;  // column c: (rhs 0, rhs 1)
+        const double2* xs0p = (const double2*)(a.xsp + q0);
+        const double2* xs1p = (const double2*)(a.xsp1 + q0);
+        const int np2 = np >> 1;
+        for (int j0 = tid; j0 < np2; j0 += kRU * kNC) {
+          double2 s0[kRU], s1[kRU];
+#pragma unroll
+          for (int u = 0; u < kRU; u++) {
+            const bool in = j0 + u * kNC < np2;
+            s0[u] = in ? __ldg(xs0p + j0 + u * kNC) : make_double2(0.0, 0.0);
+            s1[u] = in ? __ldg(xs1p + j0 + u * kNC) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < kRU; u++)
+            if (j0 + u * kNC < np2) {
+              const double2 xa = xl2[2 * (j0 + u * kNC)], xb2 = xl2[2 * (j0 + u * kNC) + 1];
+              double d = xa.x - s0[u].x;
+              acc0 = fma(d, d, acc0);
+              d = xb2.x - s0[u].y;
+              acc0 = fma(d, d, acc0);
+              d = xa.y - s1[u].x;
+              acc1 = fma(d, d, acc1);
+              d = xb2.y - s1[u].y;
+              acc1 = fma(d, d, acc1);
+            }
+        }
+        const unsigned long long* wrap = a.mbox + (size_t)(sweep & 1) * a.NB * 2;
+        const int lc1 = a.lastcol_ptr[t + 1];
+        for (int j0 = a.lastcol_ptr[t] + tid; j0 < lc1; j0 += kRU * kNC) {
+          int sl4[kRU];
+          double xs0[kRU], xs1[kRU];
+#pragma unroll
+          for (int u = 0; u < kRU; u++) {
+            const bool in = j0 + u * kNC < lc1;
+            sl4[u] = in ? __ldg(a.lastslot + j0 + u * kNC) : 0;
+            xs0[u] = in ? __ldg(a.lcx + j0 + u * kNC) : 0.0;
+            xs1[u] = in ? __ldg(a.lcx1 + j0 + u * kNC) : 0.0;
+          }
+          unsigned long long w0[kRU], w1[kRU];
+#pragma unroll
+          for (int u = 0; u < kRU; u++) {
+            const unsigned in = j0 + u * kNC < lc1 ? 1u : 0u;
+            w0[u] = ldm_if(in, wrap + 2 * (size_t)sl4[u], 0ull);
+            w1[u] = ldm_if(in, wrap + 2 * (size_t)sl4[u] + 1, 0ull);
+          }
+#pragma unroll
+          for (int u = 0; u < kRU; u++)
+            if (j0 + u * kNC < lc1) {
+              const double d0 = __longlong_as_double((long long)w0[u]) - xs0[u];
+              const double d1 = __longlong_as_double((long long)w1[u]) - xs1[u];
+              acc0 = fma(d0, d0, acc0);
+              acc1 = fma(d1, d1, acc1);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc0 += __shfl_xor_sync(kFull, acc0, o);
+          acc1 += __shfl_xor_sync(kFull, acc1, o);
+        }
+        if (lane == 0) {
+          ctl->part[warp] = acc0;
+          ctl->part[32 + warp] = acc1;
+        }
+      } else if (mode == POBK_STOP_RSE && due) {
         // columns final for this sweep once the tile's last task is done: the private ones, and
         // the shared ones whose last writer (row of the highest step) is in this tile.  x~* of the
         // private columns is contiguous per tile (16-B loads, prefetched into L2 during the
@@ -1047,10 +1353,12 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         // order) and takes the same decision -- no second, releasing hop
         const int par = (int)(sweep & 1);
         if (lane == 0) {
-          double part = 0.0;
-          if (due)
-            for (int w2 = 0; w2 < kNCW; w2++) part += ((volatile double*)ctl->part)[w2];
-          a.partials[par * a.T + t] = part;
+          for (int q = 0; q < kR; q++) {
+            double part = 0.0;
+            if (due)
+              for (int w2 = 0; w2 < kNCW; w2++) part += ((volatile double*)ctl->part)[32 * q + w2];
+            a.partials[(par * kR + q) * a.T + t] = part;
+          }
           __threadfence();
           atomicAdd(&a.sync->arrive, 1ull);
           const unsigned long long target = (unsigned long long)sweep * (unsigned long long)a.T;
@@ -1061,7 +1369,39 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         (void)ld_acquire_u64(&a.sync->arrive);  // (each lane: acquire before reading partials)
         int st = sweep >= maxs, term = POBK_TERM_MAX_SWEEPS;
         double v = 0.0;
-        if (due) {
+        if constexpr (kR == 2) {
+          // each right-hand side still iterating takes its own decision; a
+          // stopped one is frozen and keeps its record; the kernel ends when none is left
+          unsigned nact = actm;
+          for (int q = 0; q < 2; q++) {
+            if (!due || !((actm >> q) & 1u)) continue;
+            const double* pq = a.partials + (par * 2 + q) * a.T;
+            double tot = 0.0;
+            for (int b0 = 0; b0 < a.T; b0 += 32) tot += b0 + lane < a.T ? ld_cg(pq + b0 + lane) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+            const double vq = sqrt(tot) / (q ? sden1 : sden);
+            const int tq = !isfinite(vq) ? POBK_TERM_NONFINITE : (vq < tol ? POBK_TERM_CONVERGED : -1);
+            Ctrl* cq = q ? a.ctrl1 : a.ctrl;
+            if (lane == 0 && t == 0) {
+              cq->value = vq;
+              if (tq >= 0) {
+                cq->sweeps = sweep;
+                cq->term = tq;
+              }
+            }
+            if (tq >= 0) nact &= ~(1u << q);
+          }
+          if (sweep >= maxs && lane == 0 && t == 0)
+            for (int q = 0; q < 2; q++)
+              if ((nact >> q) & 1u) {
+                Ctrl* cq = q ? a.ctrl1 : a.ctrl;
+                cq->sweeps = sweep;
+                cq->term = POBK_TERM_MAX_SWEEPS;
+              }
+          st = nact == 0u || sweep >= maxs;
+          if (lane == 0) *(volatile unsigned*)&ctl->actm = nact;
+        } else if (due) {
           double tot = 0.0;  // fixed order: lane l sums tiles l, l+32, ..., then a fixed butterfly
           {  // (loads first, then the adds in the same order; T <= 160 in one round trip)
             double pv[5];
@@ -1079,7 +1419,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           else if (v < tol) { st = 1; term = POBK_TERM_CONVERGED; }
         }
         if (lane == 0) {
-          if (st && t == 0) {  // (every tile holds the same values)
+          if (kR == 1 && st && t == 0) {  // (every tile holds the same values)
             if (due) a.ctrl->value = v;
             a.ctrl->sweeps = sweep;
             a.ctrl->term = term;
@@ -1088,6 +1428,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
         }
       }
       named_bar(2, kNC);
+      if (kR > 1) actm = *(volatile unsigned*)&ctl->actm;
       if (ld_vol_shared(&ctl->stop)) {
         if (tid == 0) ctl->done = sweep;
         break;
@@ -1097,13 +1438,18 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   __syncthreads();
   for (int j = tid; j < np; j += kNT) {
     const int gcol = a.pmap[q0 + j];
-    if (gcol >= 0) a.xg[gcol] = xloc[j];
+    if (gcol >= 0) {
+      a.xg[gcol] = xloc[kR * j];
+      if (kR > 1) a.xg1[gcol] = xloc[kR * j + 1];
+    }
   }
   {  // shared columns owned by this tile: their final value sits in the last sweep's wrap slot
     const long long done = min(maxs, (long long)ctl->done);
-    const unsigned long long* wrap = a.mbox + (size_t)(done & 1) * a.NB;
-    for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNT)
-      a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + a.lastslot[j], 0ull));
+    const unsigned long long* wrap = a.mbox + (size_t)(done & 1) * a.NB * kR;
+    for (int j = a.lastcol_ptr[t] + tid; j < a.lastcol_ptr[t + 1]; j += kNT) {
+      a.xg[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + (size_t)kR * a.lastslot[j], 0ull));
+      if (kR > 1) a.xg1[a.lastcol[j]] = __longlong_as_double((long long)ldm_if(1u, wrap + (size_t)kR * a.lastslot[j] + 1, 0ull));
+    }
   }
 }
 
@@ -1131,12 +1477,13 @@ __global__ void k2_mbox_fill(unsigned long long* mbox, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     mbox[i] = kSentinel;
 }
+// (kR right-hand sides: slot s's words at kR s + q; this call seeds right-hand side q)
 __global__ void k2_mbox_seed(unsigned long long* mbox, int n, const int* __restrict__ idx, const int* __restrict__ col,
-                             const double* __restrict__ xt) {
+                             const double* __restrict__ xt, int kR, int q) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double v = xt[col[i]];
     if (v != v) v = __longlong_as_double(0x7FF8000000000000ll);  // a NaN x0 never reads as the sentinel
-    mbox[idx[i]] = (unsigned long long)__double_as_longlong(v);
+    mbox[(size_t)kR * idx[i] + q] = (unsigned long long)__double_as_longlong(v);
   }
 }
 
@@ -1151,6 +1498,7 @@ __global__ void k2_scatter_f(int64_t m, const int32_t* __restrict__ orig, const 
 struct K2Plan {
   int T = 0, NS = 0;
   int nt = 256;                // threads per CTA: 256 (BSlice2) or 512 (BSlice), see k2_build
+  int kR = 1;                  // right-hand sides per sweep (2: the two-RHS plan of pobk_solve_multi)
   size_t smem = 0;
   int nsl_max = 1, nck_max = 1, ntask_max = 1, np_max = 1;
   unsigned char* stream = nullptr;
@@ -1162,6 +1510,11 @@ struct K2Plan {
   unsigned long long* mbox = nullptr;
   double* xsp = nullptr;       // [npmap] private x~* in tile-local order
   double* lcx = nullptr;       // [nlast] owned shared columns' x~*
+  double *xsp1 = nullptr, *lcx1 = nullptr;  // (kR = 2) the second right-hand side's
+  double *xt2[2] = {nullptr, nullptr}, *xst2[2] = {nullptr, nullptr};  // (kR = 2) x~, x~* per right-hand side
+  Ctrl* ctrl2 = nullptr;       // (kR = 2) [2] device stop records
+  Ctrl* h_ctrl2 = nullptr;     // pinned mirror
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int npmap = 0, nlast = 0;
   long long NB = 0;
   int nseed = 0;
@@ -1277,7 +1630,7 @@ double private_fraction(const HostCSR& A, const std::vector<int32_t>& tile) {
 }
 }  // namespace
 
-bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why) {
+bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why, int kR) {
   if (p.any_overlap) { why = "overlapping categories"; return false; }
   int sms = 148;
   cudaDeviceProp prop;
@@ -1334,7 +1687,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
   // bytes of shared memory budgeted per private column: 8 (x~ only; the ring takes what remains,
   // at least kMinSlots slots), so that half-GPU tilings (batched solves on two lanes) stay private
   const int pcb = getenv("POBK_K2_PCB") ? std::max(8, atoi(getenv("POBK_K2_PCB"))) : 8;
-  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / pcb / 1.04) - 48;
+  const int np_cap = (int)((kSmemTotal - fixed - kMetaBudget - (size_t)kMinSlots * kSlot) / (pcb * kR) / 1.04) - 48;
   std::vector<int32_t> local(m, -1);
   std::vector<int> pmap_ptr(T + 1, 0);
   std::vector<int> pmap;
@@ -1358,7 +1711,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
   int64_t n_private_nnz = 0, n_interior = 0;
   for (int64_t i = 0; i < m; i++) {
     const int64_t len = At.ptr[i + 1] - At.ptr[i];
-    if (len > 65535 || SliceLayout(1, (int)len, true).bytes > kSlot) {
+    if (len > 65535 || SliceLayout(1, (int)len, true, kR).bytes > kSlot) {
       why = "row " + std::to_string(i) + " (" + std::to_string(len) + " nonzeros) is too long for one " +
             std::to_string(kSlot) + "-byte slice";
       return false;
@@ -1421,8 +1774,8 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         while (a < g.size()) {
           const int W = rlen(g[a]);
           size_t b = a;
-          while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd).bytes <= kSlot) b++;
-          const int R = (int)(b - a), bytes = SliceLayout(R, W, bnd).bytes;
+          while (b < g.size() && (int)(b - a) < kSliceRows && SliceLayout((int)(b - a + 1), W, bnd, kR).bytes <= kSlot) b++;
+          const int R = (int)(b - a), bytes = SliceLayout(R, W, bnd, kR).bytes;
           for (size_t r = a; r < b; r++) pad += W - rlen(g[r]);
           if (chunk_bytes + bytes > kSlot) {  // open a new chunk
             chunk_local++;
@@ -1433,7 +1786,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
           int mbase = 0;
           if (bnd) {
             const int Wp = (W + 3) & ~3;  // a lane's slots: contiguous, 32-byte aligned groups of 4
-            if (2 * (NB + (long long)Wp * R) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
+            if (2 * kR * (NB + (long long)Wp * R) >= (1LL << 31)) { why = "too many boundary entries for the mailboxes"; return false; }
             mbase = (int)NB;
             for (int r = 0; r < R; r++) mb_of_row[g[a + r]] = NB + (long long)r * Wp;
             NB += (long long)Wp * R;
@@ -1555,7 +1908,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
               bank_stats[0] / bank_stats[2], bank_stats[1] / bank_stats[2]);
   }
   const int np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
-  const size_t base_smem = fixed + meta_bytes + 8 * ((size_t)np_max + 1);  // private x~ + the zero slot
+  const size_t base_smem = fixed + meta_bytes + 8 * (size_t)kR * ((size_t)np_max + 1);  // private x~ + the zero slot
   int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
   if (getenv("POBK_K2_NS_CAP")) NS = std::min(NS, atoi(getenv("POBK_K2_NS_CAP")));  // development experiments
   if (NS < kMinSlots) { why = "shared memory too small for the TMA ring"; return false; }
@@ -1618,7 +1971,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
     const int R = (int)rows.size(), W = smeta[si].z;
     const bool bnd = slice_bnd[si];
     unsigned char* blk = stream.data() + slice_pos[si];
-    const SliceLayout L(R, W, bnd);
+    const SliceLayout L(R, W, bnd, kR);
     double* val = (double*)blk;
     double* fv = (double*)(blk + L.o_f);
     unsigned* col = (unsigned*)(blk + L.o_col);
@@ -1636,9 +1989,9 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       for (int j = rlen(i); j < W; j++) col[j * R + r] = (unsigned)np_max;  // ELL padding: zero slot, value +0
       if (bnd) ((double*)(blk + L.o_n2))[r] = nrm2[i];  // ||a~_i||^2 (row_sqnorms: the oracle's O1 order)
       len[r] = (unsigned short)rlen(i);
-      fv[r] = 0.0;  // f~ is scattered in per solve (k2_scatter_f)
+      for (int q = 0; q < kR; q++) fv[kR * r + q] = 0.0;  // f~ is scattered in per solve (k2_scatter_f)
       orig_q.push_back(p.perm[i]);
-      fslot.push_back((slice_pos[si] + L.o_f) / 8 + r);
+      fslot.push_back((slice_pos[si] + L.o_f) / 8 + (int64_t)kR * r);
     }
   }
   // Bounds check of the finished layout (every index the kernel will dereference), before upload:
@@ -1657,11 +2010,11 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         const int chunk = sm.x & 0xfffff, R = sm.x >> 20, W = sm.z;
         const int off_in = sm.y & 0xffff;
         if (tile_chunk[t] + chunk >= tile_chunk[t + 1]) return bad("slice chunk index");
-        const int bytes = SliceLayout(R, W, slice_bnd[si]).bytes;
+        const int bytes = SliceLayout(R, W, slice_bnd[si], kR).bytes;
         if (off_in + bytes > cmeta[tile_chunk[t] + chunk].y) return bad("slice outside its chunk");
         if (R < 1 || R > kSliceRows) return bad("slice rows");
         const unsigned char* blk = stream.data() + slice_pos[si];
-        const SliceLayout L(R, W, slice_bnd[si]);
+        const SliceLayout L(R, W, slice_bnd[si], kR);
         const unsigned* col = (const unsigned*)(blk + L.o_col);
         const unsigned* mout = (const unsigned*)(blk + L.o_mout);
         const unsigned short* len = (const unsigned short*)(blk + L.o_len);
@@ -1685,17 +2038,18 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
     for (int64_t i = 0; i < m; i++)
       if (!seen[i]) return bad("row " + std::to_string(i) + " never streamed");
   }
-  p.tile_of_row.assign(tile.begin(), tile.end());
+  if (kR == 1) p.tile_of_row.assign(tile.begin(), tile.end());
 
   // upload
   K2Plan* k = new K2Plan();
-  p.k2 = k;
+  (kR == 1 ? p.k2 : p.k2r) = k;
+  k->kR = kR;
   k->T = T;
   k->NS = NS;
   // CTA size: each compute warp takes about one slice per task with 7 warps when tasks are small
   // (register-resident boundary slices, 256 threads); tasks of many slices (config 5: ~16) need
   // the 15 compute warps of the 512-thread instantiation (measured: 84.6 vs 70.5 us/sweep)
-  k->nt = nt_choice;
+  k->nt = kR == 1 ? nt_choice : 256;  // (two-RHS plans: 256 threads, BSliceR2)
   k->nsl_max = nsl_max;
   k->nck_max = nck_max;
   k->ntask_max = ntask_max;
@@ -1738,27 +2092,41 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
   K2_UP(&k->lastslot, lastslot.data(), lastslot.size());
   K2_UP(&k->seed_idx, seed_idx.data(), seed_idx.size());
   K2_UP(&k->seed_col, seed_col.data(), seed_col.size());
-  K2_UP(&k->mbox, (unsigned long long*)nullptr, 2 * (size_t)std::max<long long>(NB, 1));
+  K2_UP(&k->mbox, (unsigned long long*)nullptr, 2 * (size_t)kR * std::max<long long>(NB, 1));
   K2_UP(&k->xsp, (double*)nullptr, pmap.size());
   K2_UP(&k->lcx, (double*)nullptr, lastcol.size());
+  if (kR == 2) {
+    K2_UP(&k->xsp1, (double*)nullptr, pmap.size());
+    K2_UP(&k->lcx1, (double*)nullptr, lastcol.size());
+    for (int q = 0; q < 2; q++) {
+      K2_UP(&k->xt2[q], (double*)nullptr, (size_t)m);
+      K2_UP(&k->xst2[q], (double*)nullptr, (size_t)m);
+    }
+    K2_UP(&k->ctrl2, (Ctrl*)nullptr, 2);
+    if (e == cudaSuccess) e = cudaMallocHost(&k->h_ctrl2, 2 * sizeof(Ctrl));
+    for (auto& ev : k->ev)
+      if (e == cudaSuccess) e = cudaEventCreate(&ev);
+  }
   K2_UP(&k->orig_q, orig_q.data(), orig_q.size());
   K2_UP(&k->fslot, fslot.data(), fslot.size());
   K2_UP(&k->sync, (SyncState*)nullptr, 1);
-  K2_UP(&k->partials, (double*)nullptr, 2 * (size_t)T);
+  K2_UP(&k->partials, (double*)nullptr, 2 * (size_t)kR * T);
 #undef K2_UP
   if (e != cudaSuccess) {
     why = std::string("device upload failed: ") + cudaGetErrorString(e);
-    k2_free(p);
+    if (kR == 1) k2_free(p);
+    else k2r_free(p);
     return false;
   }
-  p.ntiles = T;
+  if (kR == 1) p.ntiles = T;
   return true;
 }
 
 namespace {
 // the sweep kernel for a plan shape: threads per CTA, vector-slice width, interior mode
-const void* k2_kernel(int nt) {
-  return nt == 512 ? (const void*)k2_sweeps<512, false> : (const void*)k2_sweeps<256, true>;
+const void* k2_kernel(int nt, int kR) {
+  if (kR == 2) return (const void*)k2_sweeps<256, false, 2>;
+  return nt == 512 ? (const void*)k2_sweeps<512, false, 1> : (const void*)k2_sweeps<256, true, 1>;
 }
 }  // namespace
 
@@ -1770,7 +2138,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   k2_reset<<<1, 1, 0, s>>>(k.sync);
   k2_mbox_fill<<<148 * 4, 256, 0, s>>>(k.mbox, 2 * std::max<long long>(k.NB, 1));
   k2_mbox_seed<<<std::max(1, std::min(148 * 4, (k.nseed + 255) / 256)), 256, 0, s>>>(k.mbox, k.nseed, k.seed_idx, k.seed_col,
-                                                                                      p.d_xt);
+                                                                                      p.d_xt, 1, 0);
   launches += 4;
   if (p.d_xst && k.npmap + k.nlast > 0) {
     k2_gather_xs<<<std::max(1, std::min(148 * 4, (k.npmap + k.nlast + 255) / 256)), 256, 0, s>>>(
@@ -1798,6 +2166,10 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
   a.xst = p.d_xst;
   a.xsp = k.xsp;
   a.lcx = k.lcx;
+  a.xg1 = nullptr;
+  a.xsp1 = nullptr;
+  a.lcx1 = nullptr;
+  a.ctrl1 = nullptr;
   a.sync = k.sync;
   a.partials = k.partials;
   a.ctrl = p.d_ctrl;
@@ -1818,7 +2190,7 @@ cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& l
     a.trace_sweep = atoi(trace_env);
   }
   void* args[] = {&a};
-  const void* fn = k2_kernel(k.nt);
+  const void* fn = k2_kernel(k.nt, 1);
   if ((e = raise_smem_limit(fn)) != cudaSuccess) return e;
   e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s);
   launches++;
@@ -1851,6 +2223,165 @@ void k2_free(Plan& p) {
   if (p.k2->trace) cudaFree(p.k2->trace);
   delete p.k2;
   p.k2 = nullptr;
+}
+
+void k2r_free(Plan& p) {
+  if (!p.k2r) return;
+  for (void* v : p.k2r->allocs) cudaFree(v);
+  if (p.k2r->h_ctrl2) cudaFreeHost(p.k2r->h_ctrl2);
+  for (auto& ev : p.k2r->ev)
+    if (ev) cudaEventDestroy(ev);
+  delete p.k2r;
+  p.k2r = nullptr;
+}
+
+// The two-RHS plan (built on the first pobk_solve_multi call with R = 2 on a K2 plan): A~ in RCM
+// row order, rebuilt from the plan's device copy (storage row q is RCM row sched.rows[q]), then
+// the K2 layout with pair-interleaved x~, mailboxes and f~.
+bool k2r_build(Plan& p, std::string& why) {
+  const int64_t m = p.m, nnz = p.nnz;
+  std::vector<int32_t> rp(m + 1), col(nnz);
+  std::vector<double> val(nnz), n2s(m);
+  cudaError_t e = cudaMemcpy(rp.data(), p.A.rp, (m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(col.data(), p.A.col, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(val.data(), p.A.val, nnz * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(n2s.data(), p.A.nrm2, m * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    why = std::string("device copy failed: ") + cudaGetErrorString(e);
+    return false;
+  }
+  std::vector<int64_t> pos(m);
+  for (int64_t q = 0; q < m; q++) pos[p.sched.rows[q]] = q;
+  HostCSR At;
+  At.m = m;
+  At.ptr.assign(m + 1, 0);
+  At.col.resize(nnz);
+  At.val.resize(nnz);
+  std::vector<double> nrm2(m);
+  for (int64_t i = 0; i < m; i++) {
+    const int64_t q = pos[i], b = rp[q], len = rp[q + 1] - rp[q];
+    At.ptr[i + 1] = At.ptr[i] + len;
+    std::copy(col.begin() + b, col.begin() + b + len, At.col.begin() + At.ptr[i]);
+    std::copy(val.begin() + b, val.begin() + b + len, At.val.begin() + At.ptr[i]);
+    nrm2[i] = n2s[q];
+  }
+  return k2_build(p, At, nrm2, p.k2_tile_rows, why, 2);
+}
+
+// Two right-hand sides in one K2 launch: A~ streamed once per sweep for both; each stops on its
+// own rule and is then frozen; iterates bitwise those of the single solves.
+cudaError_t k2r_solve(Plan& p, const double* const* f, double* const* x, const double* const* xstar,
+                      const pobk_solve_opts& o, cudaStream_t s, pobk_report* reps) {
+  K2Plan& k = *p.k2r;
+  cudaError_t e;
+  long long launches = 0;
+  const bool rse = o.stop == POBK_STOP_RSE;
+  const long long ncall = o.max_sweeps - o.sweep_offset;
+  for (int q = 0; q < 2; q++) {
+    Ctrl& c = k.h_ctrl2[q];
+    c.sweeps = 0;
+    c.max_sweeps = ncall;
+    c.offset = o.sweep_offset;
+    c.tol = o.tol;
+    c.value = NAN;
+    c.den = 0.0;
+    c.stop_mode = o.stop;
+    c.check_every = o.check_every;
+    c.stopped = ncall <= 0 ? 1 : 0;
+    c.term = POBK_TERM_MAX_SWEEPS;
+    c.arrive = 0;
+    c.pad = 0;
+  }
+  if ((e = cudaEventRecord(k.ev[0], s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(k.ctrl2, k.h_ctrl2, 2 * sizeof(Ctrl), cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+  for (int q = 0; q < 2; q++) {
+    if ((e = launch_permute_in(p, nullptr, x[q], rse ? xstar[q] : nullptr, nullptr, k.xt2[q], k.xst2[q], s, launches)) !=
+        cudaSuccess)
+      return e;
+    if (rse && (e = launch_den(p, k.ctrl2 + q, k.xst2[q], s, launches)) != cudaSuccess) return e;
+  }
+  const int gf = (int)std::min<int64_t>((p.m + 255) / 256, 148 * 8);
+  for (int q = 0; q < 2; q++) k2_scatter_f<<<gf, 256, 0, s>>>(p.m, k.orig_q, k.fslot, f[q], (double*)k.stream + q);
+  k2_reset<<<1, 1, 0, s>>>(k.sync);
+  k2_mbox_fill<<<148 * 4, 256, 0, s>>>(k.mbox, 4 * std::max<long long>(k.NB, 1));
+  for (int q = 0; q < 2; q++)
+    k2_mbox_seed<<<std::max(1, std::min(148 * 4, (k.nseed + 255) / 256)), 256, 0, s>>>(k.mbox, k.nseed, k.seed_idx,
+                                                                                        k.seed_col, k.xt2[q], 2, q);
+  launches += 6;
+  if (rse && k.npmap + k.nlast > 0) {
+    const int gb = std::max(1, std::min(148 * 4, (k.npmap + k.nlast + 255) / 256));
+    k2_gather_xs<<<gb, 256, 0, s>>>(k.npmap, k.pmap, k.nlast, k.lastcol, k.xst2[0], k.xsp, k.lcx);
+    k2_gather_xs<<<gb, 256, 0, s>>>(k.npmap, k.pmap, k.nlast, k.lastcol, k.xst2[1], k.xsp1, k.lcx1);
+    launches += 2;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(k.ev[1], s)) != cudaSuccess) return e;
+  if (ncall > 0) {
+    K2Args a;
+    a.stream = k.stream;
+    a.tile_off = k.tile_off;
+    a.smeta = k.smeta;
+    a.tile_slice = k.tile_slice;
+    a.cmeta = k.cmeta;
+    a.tile_chunk = k.tile_chunk;
+    a.tmeta = k.tmeta;
+    a.tile_task = k.tile_task;
+    a.pmap_ptr = k.pmap_ptr;
+    a.pmap = k.pmap;
+    a.lastcol_ptr = k.lastcol_ptr;
+    a.lastcol = k.lastcol;
+    a.lastslot = k.lastslot;
+    a.mbox = k.mbox;
+    a.NB = k.NB;
+    a.xg = k.xt2[0];
+    a.xst = k.xst2[0];
+    a.xsp = k.xsp;
+    a.lcx = k.lcx;
+    a.xg1 = k.xt2[1];
+    a.xsp1 = k.xsp1;
+    a.lcx1 = k.lcx1;
+    a.ctrl1 = k.ctrl2 + 1;
+    a.sync = k.sync;
+    a.partials = k.partials;
+    a.ctrl = k.ctrl2;
+    a.T = k.T;
+    a.NS = k.NS;
+    a.nsl_max = k.nsl_max;
+    a.nck_max = k.nck_max;
+    a.ntask_max = k.ntask_max;
+    a.np_max = k.np_max;
+    a.trace = nullptr;
+    a.trace_sweep = -1;
+    void* args[] = {&a};
+    const void* fn = k2_kernel(k.nt, 2);
+    if ((e = raise_smem_limit(fn)) != cudaSuccess) return e;
+    if ((e = cudaLaunchCooperativeKernel(fn, dim3(k.T), dim3(k.nt), args, k.smem, s)) != cudaSuccess) return e;
+    launches++;
+  }
+  if ((e = cudaEventRecord(k.ev[2], s)) != cudaSuccess) return e;
+  for (int q = 0; q < 2; q++)
+    if ((e = launch_permute_out_from(p, k.xt2[q], x[q], s, launches)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(k.ev[3], s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(k.h_ctrl2, k.ctrl2, 2 * sizeof(Ctrl), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  float t_all = 0.f, t_sw = 0.f;
+  cudaEventElapsedTime(&t_all, k.ev[0], k.ev[3]);
+  cudaEventElapsedTime(&t_sw, k.ev[1], k.ev[2]);
+  for (int q = 0; q < 2 && reps; q++) {
+    const Ctrl& c = k.h_ctrl2[q];
+    pobk_report& rp = reps[q];
+    rp.sweeps = c.sweeps;
+    rp.termination = c.term;
+    rp.kernel = POBK_KERNEL_WAVEFRONT;
+    rp.final_value = o.stop == POBK_STOP_NONE ? NAN : c.value;
+    rp.solve_seconds = t_all * 1e-3;
+    rp.sweep_seconds = t_sw * 1e-3;
+    rp.launches = launches;
+    rp.sweeps_total = o.sweep_offset + c.sweeps;
+    rp.final_rse = rse ? c.value : NAN;
+    rp.final_relres = NAN;
+  }
+  return cudaSuccess;
 }
 
 // RELRES runs inside K2 on one-lane layouts (the residual pass reads slices in that layout)

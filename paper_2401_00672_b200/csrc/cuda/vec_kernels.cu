@@ -202,6 +202,18 @@ cudaError_t launch_permute_out(const Plan& p, double* x, cudaStream_t s, long lo
   return cudaGetLastError();
 }
 
+cudaError_t launch_permute_out_from(const Plan& p, const double* xt, double* x, cudaStream_t s, long long& launches) {
+  k_permute_out<<<grid_for(p.m), kNT, 0, s>>>(p.m, p.d_perm, xt, x);
+  launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_den(const Plan& p, Ctrl* c, const double* v, cudaStream_t s, long long& launches) {
+  k_den<<<reduce_blocks(p.m), kNT, 0, s>>>(c, p.m, v, p.d_partials);
+  launches++;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_init_ctrl(const Plan& p, const pobk_solve_opts& o, cudaStream_t s, long long& launches) {
   Ctrl* h = p.h_ctrl;
   h->sweeps = 0;

@@ -68,6 +68,8 @@ struct Plan {
   long long k1o_nodes_per_sweep = 0;
 
   K2Plan* k2 = nullptr;
+  K2Plan* k2r = nullptr;           // two right-hand sides per sweep (pobk_solve_multi, R = 2)
+  int k2_tile_rows = 0;            // the preprocess option K2 was built with (reused by k2r)
   long long pending_launches = 0;  // solve_device -> solve_finish (batched solves)
   int pending_used = 0;
   K4Plan* k4 = nullptr;
@@ -97,6 +99,9 @@ cudaError_t raise_smem_limit(const void* fn);
 cudaError_t launch_permute_in(const Plan& p, const double* f, const double* x0, const double* xstar, double* fs,
                               double* xt, double* xst, cudaStream_t s, long long& launches);
 cudaError_t launch_permute_out(const Plan& p, double* x, cudaStream_t s, long long& launches);
+cudaError_t launch_permute_out_from(const Plan& p, const double* xt, double* x, cudaStream_t s, long long& launches);
+// c->den = ||v||^2 (deterministic two-level sum)
+cudaError_t launch_den(const Plan& p, Ctrl* c, const double* v, cudaStream_t s, long long& launches);
 cudaError_t launch_init_ctrl(const Plan& p, const pobk_solve_opts& o, cudaStream_t s, long long& launches);
 cudaError_t launch_check(const Plan& p, cudaStream_t s);
 cudaError_t launch_check_graph(const Plan& p, cudaStream_t s, cudaGraphConditionalHandle h);
@@ -128,12 +133,17 @@ long long k5_nodes_per_sweep(const Plan& p);
 const BlockLayout* k5_layout(const Plan& p);
 void k5_free(Plan& p);
 // cuda/k2_wavefront.cu
-bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why);
+bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int tile_rows, std::string& why, int kR = 1);
 cudaError_t k2_solve(Plan& p, const double* f_user, cudaStream_t s, long long& launches);
 struct K2Stats { int T; double private_frac, interior_frac; long long stream_bytes; int nchunks; int threads; };
 bool k2_stats(const Plan& p, K2Stats& st);
 bool k2_relres_ok(const Plan& p);
 void k2_free(Plan& p);
+// the two-RHS K2 plan (pobk_solve_multi with R = 2 on a K2 plan): built on first use
+bool k2r_build(Plan& p, std::string& why);
+cudaError_t k2r_solve(Plan& p, const double* const* f, double* const* x, const double* const* xstar,
+                      const pobk_solve_opts& o, cudaStream_t s, pobk_report* reps);
+void k2r_free(Plan& p);
 
 }  // namespace pobk
 

@@ -543,6 +543,63 @@ def test_multi_rhs_bitwise_equals_single(env, name, n, R, tol):
     assert np.array_equal(xs[-1].cpu().numpy(), O.run_sweeps(pre, systems[-1].f, reps[-1].sweeps))
 
 
+@pytest.mark.parametrize("name,n,R,tol", [("geoknn_1m", None, 2, 0.1), ("lap3d7_64", None, 3, 0.1),
+                                          ("geoknn_1m", 60000, 5, 0.05)])
+def test_multi_rhs_wavefront_pairs(env, name, n, R, tol):
+    """K2 plans take right-hand sides in PAIRS through the two-RHS K2 layout (x~ pair-interleaved
+    in shared memory and the mailboxes, A~ streamed once per sweep for both), an
+    odd last one through the plan's own solve.  Each right-hand side keeps the per-row contract
+    and stops on its own RSE rule (a stopped one is frozen while its partner
+    iterates): stop sweep, termination, RSE value and iterates bitwise its single solve's; full
+    sizes of configs 3 and 4 (the bench's stopping point)."""
+    pk, torch = env
+    systems = [gen.make(name, b, n=n) if n else gen.make(name, b) for b in range(R)]
+    plan = pk.Plan.from_system(systems[0])
+    assert plan.layout_stats()["kernel"] == "wavefront"
+    fs = [_dev(torch, s.f) for s in systems]
+    xss = [_dev(torch, s.x_star) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = plan.solve_multi(fs, xs, xss, tol=tol)
+    assert all(r.kernel == 2 for r in reps)
+    sweeps = []
+    for s, f, xst, x, r in zip(systems, fs, xss, xs, reps):
+        x1 = _dev(torch, np.zeros(s.m))
+        r1 = plan.solve(f, x1, xst, tol=tol)
+        assert r.sweeps == r1.sweeps and r.termination == r1.termination, (r.as_dict(), r1.as_dict())
+        assert r.final_rse == r1.final_rse
+        assert np.array_equal(x.cpu().numpy(), x1.cpu().numpy())
+        sweeps.append(r.sweeps)
+    # fixed sweep count, no stop rule: the second member bitwise the oracle's sweeps
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems[:2]]
+    reps = plan.solve_multi(fs[:2], xs, None, stop="none", max_sweeps=6)
+    assert [r.sweeps for r in reps] == [6, 6] and all(r.kernel == 2 for r in reps)
+    pre = O.preprocess(systems[0].m, systems[0].indptr, systems[0].indices, systems[0].data)
+    assert np.array_equal(xs[1].cpu().numpy(), O.run_sweeps(pre, systems[1].f, 6))
+
+
+def test_multi_rhs_wavefront_freeze(env):
+    """A two-RHS K2 solve whose members stop far apart: RHS 0 starts from an x0 close to x*, so it
+    meets the RSE rule early and stays frozen while RHS 1 (x0 = 0) iterates on; each matches its
+    own single solve bitwise (stop sweep and iterates)."""
+    pk, torch = env
+    s = gen.make("geoknn_1m", 0, n=30000)
+    plan = pk.Plan.from_system(s)
+    assert plan.layout_stats()["kernel"] == "wavefront"
+    f, xst = _dev(torch, s.f), _dev(torch, s.x_star)
+    x0 = _dev(torch, s.x_star * 0.999)
+    xs = [x0.clone(), _dev(torch, np.zeros(s.m))]
+    r2 = plan.solve_multi([f, f], xs, [xst, xst], tol=0.01)
+    xa = x0.clone()
+    ra = plan.solve(f, xa, xst, tol=0.01)
+    xb = _dev(torch, np.zeros(s.m))
+    rb = plan.solve(f, xb, xst, tol=0.01)
+    assert ra.sweeps < rb.sweeps, (ra.sweeps, rb.sweeps)
+    assert (r2[0].sweeps, r2[1].sweeps) == (ra.sweeps, rb.sweeps)
+    assert r2[0].final_rse == ra.final_rse and r2[1].final_rse == rb.final_rse
+    assert np.array_equal(xs[0].cpu().numpy(), xa.cpu().numpy())
+    assert np.array_equal(xs[1].cpu().numpy(), xb.cpu().numpy())
+
+
 def test_multi_rhs_contract(env):
     pk, torch = env
     s = gen.make("lap2d5_32")
