@@ -494,6 +494,7 @@ struct BSlice {
                                        unsigned long long* trp) {
     constexpr int kG = 4;
     const double n2 = lds64(S.vb + (unsigned)SliceLayout(R, W, true).o_n2);  // (vb = block + 8 * lane)
+    const double y2 = rcp_ahead(n2);  // (independent of the row sum: overlaps it)
     double s = 0.0;
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kG) {
@@ -542,7 +543,7 @@ struct BSlice {
       __syncwarp();
       if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
     }
-    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+    const double alpha = div_by_rcp(__dsub_rn(S.f, s), n2, y2);
     if (trp) {
       double a2 = alpha;
       asm volatile("mov.b64 %0, %0;" : "+d"(a2));
@@ -603,7 +604,7 @@ struct BSlice2 {
   double av[kMaxJ];
   unsigned tg[kMaxJ];
   unsigned shm, prv;  // bit j: entry j is a real shared entry / a private entry (incl. ELL padding)
-  double n2;
+  double n2, y2;  // ||a~||^2 and RN(1/||a~||^2) (the division's reciprocal, formed in the look-ahead)
   __device__ __forceinline__ void pre(const SliceAddr& S, int W, int R, int lane, unsigned blk, unsigned xb) {
     shm = 0u;
     prv = 0u;
@@ -611,6 +612,7 @@ struct BSlice2 {
       const SliceLayout Ly(R, W, true);
       n2 = lds64(blk + (unsigned)Ly.o_n2 + 8u * (lane < R ? lane : 0));
     }
+    y2 = rcp_ahead(n2);
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kBatch) {
       if (jb < W) {
@@ -713,7 +715,7 @@ struct BSlice2 {
       __syncwarp();
       if ((threadIdx.x & 31) == 0) trp[2] = gtimer();
     }
-    const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+    const double alpha = div_by_rcp(__dsub_rn(S.f, s), n2, y2);
     if (trp) {
       double a2 = alpha;
       asm volatile("mov.b64 %0, %0;" : "+d"(a2));
@@ -788,7 +790,8 @@ __device__ __forceinline__ void slice_interior2(const SliceAddr& S, int W, unsig
       n2 = __dadd_rn(n2, qq[u]);
     }
   }
-  const double al0 = __ddiv_rn(__dsub_rn(S.f, s0), n2), al1 = __ddiv_rn(__dsub_rn(S.f1, s1), n2);
+  const double y2 = rcp_ahead(n2);  // (one reciprocal for both quotients)
+  const double al0 = div_by_rcp(__dsub_rn(S.f, s0), n2, y2), al1 = div_by_rcp(__dsub_rn(S.f1, s1), n2, y2);
   for (int jb = 0; jb < W; jb += kIB) {
     unsigned c[kIB];
     double av[kIB];
@@ -855,6 +858,7 @@ struct BSliceR2 {
                                        unsigned long long* mbox, unsigned off_p, unsigned off_q, unsigned act) {
     constexpr int kG = 4;
     const double n2 = lds64(S.vb + (unsigned)SliceLayout(R, W, true, 2).o_n2);  // (vb = block + 8 * lane)
+    const double y2 = rcp_ahead(n2);  // (independent of the row sums: overlaps them)
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kG) {
@@ -905,7 +909,7 @@ struct BSliceR2 {
       s0 = __dadd_rn(s0, __dmul_rn(a, x0));
       s1 = __dadd_rn(s1, __dmul_rn(a, x1));
     }
-    const double al0 = __ddiv_rn(__dsub_rn(S.f, s0), n2), al1 = __ddiv_rn(__dsub_rn(S.f1, s1), n2);
+    const double al0 = div_by_rcp(__dsub_rn(S.f, s0), n2, y2), al1 = div_by_rcp(__dsub_rn(S.f1, s1), n2, y2);
 #pragma unroll
     for (int jb = 0; jb < kMaxJ; jb += kG) {
       if (jb < W) {
@@ -1875,6 +1879,56 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         res[x] = best;
         csize[best]++;
         for (int g : groups_of[x]) cnt[(size_t)g * 16 + best]++;
+      }
+      // local search on the modelled cost itself: an access group (slice, entry, half warp) takes
+      // max(1, max_k members with residue k) wavefronts; move a column to the residue that lowers
+      // the sum over its groups the most (capacity permitting), a few passes
+      {
+        const int passes = getenv("POBK_K2_BANKPASS") ? atoi(getenv("POBK_K2_BANKPASS")) : 4;
+        std::vector<uint8_t> gmax(ng, 0);
+        for (int g = 0; g < ng; g++) {
+          uint8_t mx = 0;
+          for (int k = 0; k < 16; k++) mx = std::max(mx, cnt[(size_t)g * 16 + k]);
+          gmax[g] = mx;
+        }
+        std::vector<int> mr;  // per group of x: max over residues with x removed
+        for (int pass = 0; pass < passes; pass++) {
+          long moved = 0;
+          for (int x : order) {
+            const int r = res[x];
+            const auto& G = groups_of[x];
+            if (G.empty()) continue;
+            mr.resize(G.size());
+            long cur = 0;
+            for (size_t q = 0; q < G.size(); q++) {
+              const uint8_t* c = &cnt[(size_t)G[q] * 16];
+              int mx = 0;
+              for (int k = 0; k < 16; k++) mx = std::max(mx, (int)c[k] - (k == r ? 1 : 0));
+              mr[q] = mx;
+              cur += std::max(1, (int)gmax[G[q]]);
+            }
+            int best = r;
+            long best_cost = cur;
+            for (int k = 0; k < 16; k++) {
+              if (k == r || csize[k] >= cap) continue;
+              long cost = 0;
+              for (size_t q = 0; q < G.size(); q++) cost += std::max(1, std::max(mr[q], (int)cnt[(size_t)G[q] * 16 + k] + 1));
+              if (cost < best_cost) { best_cost = cost; best = k; }
+            }
+            if (best == r) continue;
+            for (size_t q = 0; q < G.size(); q++) {
+              uint8_t* c = &cnt[(size_t)G[q] * 16];
+              c[r]--;
+              c[best]++;
+              gmax[G[q]] = (uint8_t)std::max(mr[q], (int)c[best]);
+            }
+            csize[r]--;
+            csize[best]++;
+            res[x] = best;
+            moved++;
+          }
+          if (moved == 0) break;
+        }
       }
       if (getenv("POBK_K2_BANKSTATS")) {  // development aid: modelled wavefronts per x~ access
         double& acc_new = bank_stats[0]; double& acc_old = bank_stats[1]; double& acc_n = bank_stats[2];

@@ -143,7 +143,7 @@ struct K3EArgs {
 };
 
 size_t k3e_bytes(int m, int nent, int nsteps) {
-  return align16(8ull * nent) + align16(4ull * nent) + align16(8ull * (m + 1)) + 3 * align16(8ull * m) +
+  return align16(8ull * nent) + align16(4ull * nent) + align16(8ull * (m + 1)) + 4 * align16(8ull * m) +
          align16(16ull * nsteps) + 64 * 8;
 }
 
@@ -151,7 +151,7 @@ size_t k3e_bytes(int m, int nent, int nsteps) {
 // value +0) selected without branches, so all operand loads of the row issue back to back.
 template <int EW>
 __device__ __forceinline__ void k3e_row(const int32_t* col, const double* val, double* x, int e0, int W, double fi,
-                                        double ni, int m) {
+                                        double ni, double yi, int m) {
   int c[EW];
   double av[EW], xv[EW];
 #pragma unroll
@@ -169,7 +169,7 @@ __device__ __forceinline__ void k3e_row(const int32_t* col, const double* val, d
   for (int j = 0; j < EW; j++) pp[j] = pin(__dmul_rn(av[j], xv[j]));  // products first (common.cuh)
 #pragma unroll
   for (int j = 0; j < EW; j++) sum = __dadd_rn(sum, pp[j]);  // (+0 * +0 past W: no-ops)
-  const double alpha = __ddiv_rn(__dsub_rn(fi, sum), ni);
+  const double alpha = div_by_rcp(__dsub_rn(fi, sum), ni, yi);  // (= __ddiv_rn: common.cuh)
 #pragma unroll
   for (int j = 0; j < EW; j++)
     if (c[j] < m) x[c[j]] = __dadd_rn(xv[j], __dmul_rn(alpha, av[j]));
@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
   double* xs = (double*)take(8ull * a.m);
   double* f = (double*)take(8ull * a.m);
   double* nrm2 = (double*)take(8ull * a.m);
+  double* rn = (double*)take(8ull * a.m);  // RN(1/nrm2): the division's reciprocal, formed once
   int4* info = (int4*)take(16ull * a.nsteps);
   double* red = (double*)take(64 * 8);
 
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
     xs[i] = a.xst ? a.xst[i] : 0.0;
     f[i] = a.fs[i];
     nrm2[i] = a.nrm2[i];
+    rn[i] = rcp_ahead(a.nrm2[i]);
   }
   for (int i = tid; i < a.nsteps; i += kENT) info[i] = ((const int4*)a.einfo)[i];
   if (tid == 0) x[a.m] = 0.0;  // the zero slot of the ELL padding (never written)
@@ -218,8 +220,8 @@ __global__ void __launch_bounds__(kENT, 1) k3e_sweeps(K3EArgs a) {
         if (rr < in.y) {
           const int sidx = in.x + rr, W = in.z;
           const int e0 = in.w + (r0 / kENT) * W * kENT + tid;
-          if (W <= 8) k3e_row<8>(col, val, x, e0, W, f[sidx], nrm2[sidx], a.m);
-          else k3e_row<kEW>(col, val, x, e0, W, f[sidx], nrm2[sidx], a.m);
+          if (W <= 8) k3e_row<8>(col, val, x, e0, W, f[sidx], nrm2[sidx], rn[sidx], a.m);
+          else k3e_row<kEW>(col, val, x, e0, W, f[sidx], nrm2[sidx], rn[sidx], a.m);
         }
       }
       __syncthreads();
