@@ -114,6 +114,43 @@ pobk_status build_device(Plan& p, const HostCSR& At, const std::vector<double>& 
   CUDA_TRY(dalloc(p, &p.d_xst, m));
   CUDA_TRY(dalloc(p, &p.d_fs, m));
   CUDA_TRY(dalloc(p, &p.d_alpha, p.any_overlap ? max_step : 1));
+  if (p.any_overlap) {  // per overlapping step, its entries by column (ascending schedule position)
+    std::vector<int32_t> cols, eptr(1, 0), es;
+    std::vector<double> ev;
+    std::vector<int32_t> cnt(m, 0), first(m, -1);
+    p.h_ov_colptr.assign(p.nsteps + 1, 0);
+    for (int32_t k = 0; k < p.nsteps; k++) {
+      p.h_ov_colptr[k] = (int32_t)cols.size();
+      if (!p.h_overlap[k]) continue;
+      const int32_t s0 = p.h_step_ptr[k], s1 = p.h_step_ptr[k + 1];
+      const size_t c0 = cols.size();
+      for (int32_t s = s0; s < s1; s++)
+        for (int32_t q = rp[s]; q < rp[s + 1]; q++) {
+          const int32_t c = col[q];
+          if (cnt[c]++ == 0) cols.push_back(c);
+        }
+      const size_t e0 = es.size();
+      for (size_t t = c0; t < cols.size(); t++) {  // offsets (entries of the step's columns, in cols order)
+        first[cols[t]] = (int32_t)(eptr.back());
+        eptr.push_back(eptr.back() + cnt[cols[t]]);
+      }
+      es.resize(e0 + (size_t)(eptr.back() - (int32_t)e0));
+      ev.resize(es.size());
+      for (int32_t s = s0; s < s1; s++)  // ascending s: each column's entries in schedule order
+        for (int32_t q = rp[s]; q < rp[s + 1]; q++) {
+          const int32_t c = col[q];
+          es[first[c]] = s - s0;
+          ev[first[c]++] = val[q];
+        }
+      for (size_t t = c0; t < cols.size(); t++) cnt[cols[t]] = 0;
+    }
+    p.h_ov_colptr[p.nsteps] = (int32_t)cols.size();
+    CUDA_TRY(upload(p, &p.ov_colptr, p.h_ov_colptr.data(), p.h_ov_colptr.size()));
+    CUDA_TRY(upload(p, &p.ov_cols, cols.data(), std::max<size_t>(cols.size(), 1)));
+    CUDA_TRY(upload(p, &p.ov_eptr, eptr.data(), eptr.size()));
+    CUDA_TRY(upload(p, &p.ov_es, es.data(), std::max<size_t>(es.size(), 1)));
+    CUDA_TRY(upload(p, &p.ov_ev, ev.data(), std::max<size_t>(ev.size(), 1)));
+  }
   CUDA_TRY(dalloc(p, &p.d_partials, kMaxReduceBlocks));
   CUDA_TRY(dalloc(p, &p.d_ctrl, 1));
   CUDA_TRY(cudaMemset(p.d_ctrl, 0, sizeof(Ctrl)));

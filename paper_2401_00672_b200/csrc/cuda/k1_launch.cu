@@ -5,12 +5,14 @@
 // collapses by Lemma 1 to independent Eq 1.2 row projections
 // (PAPER.md:29): one thread per row (common.cuh contract), no atomics (disjoint supports), the
 // launch boundary is the step barrier.  Steps whose rows overlap (thr > 0 only) run as two
-// launches: all alphas at the same x~, then an fp64-atomic scatter.
+// launches: all alphas at the same x~, then the scatter as an ordered fold per column (bitwise the
+// oracle's; POBK_THR_ATOMIC=1: an fp64-atomic scatter, order nondeterministic).
 //
 // The sweep loop is device-driven: the steps + the stop check are the body of a CUDA-graph WHILE
 // node whose condition the check kernel clears (no host round trip per sweep).  K1 is the
 // general fallback (any size, any thr); K2/K3 are the fast paths.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "../plan.h"
@@ -49,7 +51,24 @@ __global__ void __launch_bounds__(kNT) k1_scatter_atomic(const int32_t* __restri
   for (int p = rp[s]; p < rp[s + 1]; p++) atomicAdd(x + col[p], __dmul_rn(a, val[p]));
 }
 
+// pass 2, ordered (default): one thread per column the step touches, folding the step's
+// contributions in ascending schedule position -- x~_c = (x~_c + alpha_i1 a~_i1c) + alpha_i2 a~_i2c
+// ..., each product and sum rounded, which is the oracle's order (rows ascending, entries
+// ascending): bitwise the oracle's iterates, no atomics
+__global__ void __launch_bounds__(kNT) k1_scatter_ordered(const int32_t* __restrict__ cols, const int32_t* __restrict__ eptr,
+                                                          const int32_t* __restrict__ es, const double* __restrict__ ev,
+                                                          const double* __restrict__ alpha, double* __restrict__ x, int c0,
+                                                          int c1) {
+  const int t = c0 + blockIdx.x * kNT + threadIdx.x;
+  if (t >= c1) return;
+  const int c = cols[t];
+  double xc = x[c];
+  for (int e = eptr[t]; e < eptr[t + 1]; e++) xc = __dadd_rn(xc, __dmul_rn(alpha[es[e]], ev[e]));
+  x[c] = xc;
+}
+
 cudaError_t capture_sweep(Plan& p, cudaStream_t cs, long long& nodes) {
+  const bool atomic = getenv("POBK_THR_ATOMIC") != nullptr;  // the fp64-atomic scatter (order nondeterministic)
   for (int k = 0; k < p.nsteps; k++) {
     const int s0 = p.h_step_ptr[k], s1 = p.h_step_ptr[k + 1];
     const int grid = (s1 - s0 + kNT - 1) / kNT;
@@ -58,7 +77,13 @@ cudaError_t capture_sweep(Plan& p, cudaStream_t cs, long long& nodes) {
       nodes++;
     } else {
       k1_alpha<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, p.d_alpha, s0, s1);
-      k1_scatter_atomic<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_alpha, p.d_xt, s0, s1);
+      if (atomic) {
+        k1_scatter_atomic<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_alpha, p.d_xt, s0, s1);
+      } else {
+        const int c0 = p.h_ov_colptr[k], c1 = p.h_ov_colptr[k + 1];
+        k1_scatter_ordered<<<(c1 - c0 + kNT - 1) / kNT, kNT, 0, cs>>>(p.ov_cols, p.ov_eptr, p.ov_es, p.ov_ev, p.d_alpha,
+                                                                     p.d_xt, c0, c1);
+      }
       nodes += 2;
     }
   }

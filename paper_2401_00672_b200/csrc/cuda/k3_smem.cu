@@ -25,6 +25,10 @@ struct K3Args {
   const double* fs;
   const int32_t* step_ptr;  // [nsteps+1]
   const uint8_t* overlap;   // [nsteps]
+  // overlapping steps: entries by column (plan.h ov_*), the ordered scatter; atomic: fp64 atomics
+  const int32_t *ov_colptr, *ov_cols, *ov_eptr, *ov_es;
+  const double* ov_ev;
+  int atomic;
   double* xt;
   const double* xst;
   Ctrl* ctrl;
@@ -84,8 +88,17 @@ __global__ void __launch_bounds__(kNT, 1) k3_sweeps(K3Args a) {
         for (int s = s0 + tid; s < s1; s += kNT)
           alpha[s - s0] = __ddiv_rn(__dsub_rn(f[s], row_dot(col, val, rp[s], rp[s + 1], x)), nrm2[s]);
         __syncthreads();
-        for (int s = s0 + tid; s < s1; s += kNT)
-          for (int p = rp[s]; p < rp[s + 1]; p++) atomicAdd(x + col[p], __dmul_rn(alpha[s - s0], val[p]));
+        if (a.atomic) {
+          for (int s = s0 + tid; s < s1; s += kNT)
+            for (int p = rp[s]; p < rp[s + 1]; p++) atomicAdd(x + col[p], __dmul_rn(alpha[s - s0], val[p]));
+        } else {  // one thread per column: the step's contributions in ascending row order (the oracle's)
+          for (int t = a.ov_colptr[k] + tid; t < a.ov_colptr[k + 1]; t += kNT) {
+            const int c = a.ov_cols[t];
+            double xc = x[c];
+            for (int e = a.ov_eptr[t]; e < a.ov_eptr[t + 1]; e++) xc = __dadd_rn(xc, __dmul_rn(alpha[a.ov_es[e]], a.ov_ev[e]));
+            x[c] = xc;
+          }
+        }
       }
       __syncthreads();
     }
@@ -313,6 +326,12 @@ cudaError_t launch(Plan& p, cudaStream_t s) {
   a.fs = p.d_fs;
   a.step_ptr = p.k3_step_ptr;
   a.overlap = p.k3_overlap;
+  a.ov_colptr = p.ov_colptr;
+  a.ov_cols = p.ov_cols;
+  a.ov_eptr = p.ov_eptr;
+  a.ov_es = p.ov_es;
+  a.ov_ev = p.ov_ev;
+  a.atomic = getenv("POBK_THR_ATOMIC") != nullptr;
   a.xt = p.d_xt;
   a.xst = p.d_xst;
   a.ctrl = p.d_ctrl;

@@ -51,6 +51,15 @@ struct Plan {
   double* d_xst = nullptr;        // [m] x~* (RCM frame)
   double* d_fs = nullptr;         // [m] f~ in storage order
   double* d_alpha = nullptr;      // [max step size] thr > 0 scratch
+  // thr > 0, overlapping steps: the step's entries grouped by column (CSC over its schedule
+  // positions, ascending), so the scatter x~_c += sum_i alpha_i a~_ic is one fold per column in
+  // the oracle's order (bitwise) -- no atomics (POBK_THR_ATOMIC=1: the fp64-atomic scatter)
+  std::vector<int32_t> h_ov_colptr;  // [nsteps+1] offsets into ov_cols (empty range: disjoint step)
+  int32_t* ov_colptr = nullptr;   // device copy of h_ov_colptr (K3)
+  int32_t* ov_cols = nullptr;     // [ncols] the columns each overlapping step touches
+  int32_t* ov_eptr = nullptr;     // [ncols+1] offsets into ov_es / ov_ev
+  int32_t* ov_es = nullptr;       // [entries] step-local row index (the alpha slot), ascending per column
+  double* ov_ev = nullptr;        // [entries] a~_ic
   double* d_partials = nullptr;   // [kMaxReduceBlocks]
   Ctrl* d_ctrl = nullptr;
   Ctrl* h_ctrl = nullptr;         // pinned mirror

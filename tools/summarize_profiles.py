@@ -18,7 +18,7 @@ for r in rows:
     by[name][1] += float(r[14]) * (1e-3 if r[13] == "ns" else 1.0)   # -> us
 tot = sum(v[1] for v in by.values())
 out = [f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`) of "
-       f"`python bench.py --steps 2 --warmup 1 --no-cpu-baseline` ({workload})", "",
+       f"`python bench.py --steps 2 --warmup 3 --no-cpu-baseline` ({workload})", "",
        "Cold-cache, serialised per-launch times: compare SHARES, not absolutes.", "",
        "| kernel | launches | total us | share |", "|---|---:|---:|---:|"]
 for k, (n, us) in sorted(by.items(), key=lambda kv: -kv[1][1]):
