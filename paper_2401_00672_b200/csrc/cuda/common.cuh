@@ -8,8 +8,9 @@
 //     for p:  x_{col p} = x_{col p} + (alpha * a_p)                (dmul_rn, then dadd_rn)
 // Because the rows of one category have disjoint supports (thr = 0), the order in which a
 // category's rows are applied cannot change any value, so every kernel family reproduces the
-// oracle's iterates BIT FOR BIT, whatever its parallel schedule.  (thr > 0 overlapping categories
-// use fp64 atomics for the scatter: order-dependent, parity to 1e-9.)
+// oracle's iterates BIT FOR BIT, whatever its parallel schedule.  (thr > 0 overlapping categories:
+// every alpha first, then per column x_c = x_c + (alpha_i * a_ic) in ascending row order -- the
+// oracle's order, also bitwise; POBK_THR_ATOMIC=1 switches to fp64 atomics, parity to 1e-9.)
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
