@@ -96,6 +96,9 @@ constexpr int kWB = POBK_K2_WB;
 #define POBK_K2_RSEU 4
 #endif
 constexpr int kRU = POBK_K2_RSEU;  // end-of-sweep RSE scan: loads in flight per thread  // boundary write-back: entries issued per group  // boundary row sum: products of a group first, then its adds
+#ifndef POBK_K2_TMEM
+#define POBK_K2_TMEM 1  // interior pass-2 operands in tensor memory (measured r02f: config 4 96.8 -> 93.7 us/sweep)
+#endif
 #ifndef POBK_K2_IBATCH
 #define POBK_K2_IBATCH 4  // (measured r02: 4 vs 8 -- config 4 97.6 vs 98.1 us/sweep, config 5 200.6 vs 190.3 G)
 #endif
@@ -433,6 +436,72 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
     for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
     for (int u = 0; u < kIB; u++) sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv[u], __dmul_rn(alpha, av[u])));
+  }
+}
+
+// interior slice with pass 1's operands parked in tensor memory (TMEM) for pass 2: pass 2 reads
+// them back with tcgen05.ld (own datapath) instead of re-reading col, value and x~ from shared
+// memory -- the shared-memory pipe keeps only pass 1's loads and pass 2's x~ stores.
+// taddr: this warp's TMEM region (its lane quarter, 20 columns per 4-entry batch); W <= kTmMaxW.
+__device__ __forceinline__ void tm_st4(unsigned a, unsigned v0, unsigned v1, unsigned v2, unsigned v3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v0), "r"(v1), "r"(v2), "r"(v3)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(unsigned a, unsigned& v0, unsigned& v1, unsigned& v2, unsigned& v3) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+               : "r"(a)
+               : "memory");
+}
+__device__ __forceinline__ void slice_interior_tm(const SliceAddr& S, int W, unsigned xb, unsigned taddr) {
+  static_assert(kIB == 4, "slice_interior_tm parks 4-entry batches (20 TMEM columns each)");
+  double s = 0.0, n2 = 0.0;
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB], xv[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    const unsigned ta = taddr + (unsigned)(jb / kIB) * 20u;
+    tm_st4(ta, c[0], c[1], c[2], c[3]);
+    tm_st4(ta + 4, __double2loint(av[0]), __double2hiint(av[0]), __double2loint(av[1]), __double2hiint(av[1]));
+    tm_st4(ta + 8, __double2loint(av[2]), __double2hiint(av[2]), __double2loint(av[3]), __double2hiint(av[3]));
+    tm_st4(ta + 12, __double2loint(xv[0]), __double2hiint(xv[0]), __double2loint(xv[1]), __double2hiint(xv[1]));
+    tm_st4(ta + 16, __double2loint(xv[2]), __double2hiint(xv[2]), __double2loint(xv[3]), __double2hiint(xv[3]));
+    double pp[kIB], qq[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const bool in = jb + u < W;
+      const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
+      pp[u] = pin(__dmul_rn(a, x));
+      qq[u] = pin(__dmul_rn(a, a));
+    }
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      s = __dadd_rn(s, pp[u]);
+      n2 = __dadd_rn(n2, qq[u]);
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
+  for (int jb = 0; jb < W; jb += kIB) {
+    const unsigned ta = taddr + (unsigned)(jb / kIB) * 20u;
+    unsigned c[kIB], w[16];
+    tm_ld4(ta, c[0], c[1], c[2], c[3]);
+    tm_ld4(ta + 4, w[0], w[1], w[2], w[3]);
+    tm_ld4(ta + 8, w[4], w[5], w[6], w[7]);
+    tm_ld4(ta + 12, w[8], w[9], w[10], w[11]);
+    tm_ld4(ta + 16, w[12], w[13], w[14], w[15]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const double av = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]);
+      const double xv = __hiloint2double((int)w[8 + 2 * u + 1], (int)w[8 + 2 * u]);
+      sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv, __dmul_rn(alpha, av)));
+    }
   }
 }
 
@@ -966,6 +1035,11 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kNCW = kNT / 32 - 1;  // compute warps; warp kNCW is the TMA producer
   constexpr int kNC = kNCW * 32;      // compute threads
   constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
+  // interior slices park pass 1's operands in TMEM for pass 2 (slice_interior_tm): each warp owns
+  // a TMEM region of its lane quarter (warp % 4), 512 / (warps per quarter) columns wide
+  constexpr bool kTM = kR == 1 && POBK_K2_TMEM;
+  constexpr int kTmCols = 512 / ((kNT / 32 + 3) / 4);        // columns per warp region (256 / 128)
+  constexpr int kTmMaxW = (kTmCols / 20) * kIB;              // widest slice whose operands fit (20 columns per 4 entries)
   extern __shared__ __align__(128) unsigned char smem[];
   const int NS = a.NS;
   unsigned char* ring = smem;                                // NS * kSlot
@@ -1009,7 +1083,15 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
     xloc[kR * j] = gcol >= 0 ? a.xg[gcol] : 0.0;
     if (kR > 1) xloc[kR * j + 1] = gcol >= 0 ? a.xg1[gcol] : 0.0;
   }
+  __shared__ unsigned s_tmem;
+  if (kTM && warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (kTM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (kTM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem_w = kTM ? s_tmem + ((32u * (unsigned)(warp & 3)) << 16) + (unsigned)((warp >> 2) * kTmCols) : 0u;
 
   if (warp == kNCW) {
     // ================================================================ producer warp (TMA only)
@@ -1157,7 +1239,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
           } else if constexpr (kR == 2) {
             slice_interior2(S, W, xb, actm);
           } else {
-            slice_interior(S, W, xb);
+            if (kTM && W <= kTmMaxW) slice_interior_tm(S, W, xb, tmem_w);
+            else slice_interior(S, W, xb);
           }
           __syncwarp();
           if (lane == 0) atomicAdd(&ctl->released[slot], 1);
@@ -1439,7 +1522,12 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
       }
     }
   }
+  if (kTM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (kTM && warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+  }
   for (int j = tid; j < np; j += kNT) {
     const int gcol = a.pmap[q0 + j];
     if (gcol >= 0) {
