@@ -113,7 +113,7 @@ constexpr unsigned kFull = 0xffffffffu;
 __host__ __device__ inline int a16(long long b) { return (int)((b + 15) & ~15LL); }
 
 // slice block (bytes): val[W*R] f[R*nf] (fp64; nf right-hand sides, row-major) | [boundary slices] n2[R] (fp64: ||a~||^2)
-//                      | col[W*R] (u32: shared flag | index)
+//                      | col[W*R] (boundary slices: u32 shared flag | index; interior slices: u16 local index)
 //                      | [boundary slices] mout[W*R] (u32: wrap flag | mailbox index) | len[R] (u16)
 struct SliceLayout {
   int o_f, o_n2, o_col, o_mout, o_len, bytes;
@@ -121,7 +121,7 @@ struct SliceLayout {
     o_f = 8 * W * R;
     o_n2 = o_f + 8 * R * nf;
     o_col = o_n2 + (bnd ? 8 * R : 0);
-    o_mout = o_col + 4 * W * R;
+    o_mout = o_col + (bnd ? 4 : 2) * W * R;
     o_len = o_mout + (bnd ? 4 * W * R : 0);
     bytes = a16(o_len + 2 * R);
   }
@@ -375,17 +375,17 @@ __device__ __forceinline__ void lds64x4_if(double& v0, double& v1, double& v2, d
 // is never -0); only the stores are predicated on j < len_r.  Rows are applied with the per-row
 // contract of common.cuh (Eq 1.2).
 struct SliceAddr {
-  unsigned vb, cb, mb;  // this lane's val / col / mout entry 0; entry j at + j*R*8 / + j*R*4
+  unsigned vb, cb, mb;  // this lane's val / col / mout entry 0; entry j at + j*vs / + j*cs (u32 col, boundary) or u16 col (interior)
   unsigned vs, cs;      // strides
   int myl;              // row length (0 for lanes >= R)
   double f, f1;         // f~_i (f1: the second right-hand side's, nf = 2)
   __device__ __forceinline__ SliceAddr(unsigned blk, int R, int W, bool bnd, int lane, int nf = 1) {
     const int ln = lane < R ? lane : 0;
     vs = 8u * R;
-    cs = 4u * R;
+    cs = (bnd ? 4u : 2u) * R;
     const SliceLayout L(R, W, bnd, nf);
     vb = opaque(blk + 8u * ln);
-    cb = opaque(blk + (unsigned)L.o_col + 4u * ln);
+    cb = opaque(blk + (unsigned)L.o_col + (bnd ? 4u : 2u) * ln);
     mb = blk + (unsigned)L.o_mout + 4u * ln;
     f = lds64(blk + (unsigned)L.o_f + 8u * nf * ln);
     f1 = nf > 1 ? lds64(blk + (unsigned)L.o_f + 8u * nf * ln + 8u) : 0.0;
@@ -401,7 +401,7 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
     unsigned c[kIB];
     double av[kIB], xv[kIB];
 #pragma unroll
-    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+    for (int u = 0; u < kIB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
     for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
@@ -429,7 +429,7 @@ __device__ __forceinline__ void slice_interior(const SliceAddr& S, int W, unsign
     double av[kIB], xv[kIB];
 #pragma unroll
     for (int u = 0; u < kIB; u++) {
-      c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+      c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
       av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
     }
 #pragma unroll
@@ -460,7 +460,7 @@ __device__ __forceinline__ void slice_interior_tm(const SliceAddr& S, int W, uns
     unsigned c[kIB];
     double av[kIB], xv[kIB];
 #pragma unroll
-    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+    for (int u = 0; u < kIB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
     for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
@@ -838,7 +838,7 @@ __device__ __forceinline__ void slice_interior2(const SliceAddr& S, int W, unsig
     double av[kIB];
     double2 xv[kIB];
 #pragma unroll
-    for (int u = 0; u < kIB; u++) c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+    for (int u = 0; u < kIB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
     for (int u = 0; u < kIB; u++) xv[u] = lds128(xb + 16u * c[u]);
 #pragma unroll
@@ -867,7 +867,7 @@ __device__ __forceinline__ void slice_interior2(const SliceAddr& S, int W, unsig
     double2 xv[kIB];
 #pragma unroll
     for (int u = 0; u < kIB; u++) {
-      c[u] = lds32(S.cb + min(jb + u, W - 1) * S.cs);
+      c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
       av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
     }
 #pragma unroll
@@ -1298,7 +1298,7 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             if (lane < R) {
               double sr = 0.0;
               for (int j = 0; j < W; j++) {
-                const unsigned c = lds32(S.cb + j * S.cs);
+                const unsigned c = q < nbnd ? lds32(S.cb + j * S.cs) : lds16(S.cb + j * S.cs);
                 const double av = lds64(S.vb + j * S.vs);
                 const double xv = (c & kShared) ? ld_cg(a.xg + (c & kIdx)) : lds64(xb + 8u * c);
                 sr = __dadd_rn(sr, __dmul_rn(av, xv));
@@ -1971,8 +1971,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       // local search on the modelled cost itself: an access group (slice, entry, half warp) takes
       // max(1, max_k members with residue k) wavefronts; move a column to the residue that lowers
       // the sum over its groups the most (capacity permitting), a few passes
-      {
-        const int passes = getenv("POBK_K2_BANKPASS") ? atoi(getenv("POBK_K2_BANKPASS")) : 4;
+      auto col_ls = [&](int passes) {
         std::vector<uint8_t> gmax(ng, 0);
         for (int g = 0; g < ng; g++) {
           uint8_t mx = 0;
@@ -2017,7 +2016,9 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
           }
           if (moved == 0) break;
         }
-      }
+      };
+      const int cpasses = getenv("POBK_K2_BANKPASS") ? atoi(getenv("POBK_K2_BANKPASS")) : 4;
+      col_ls(cpasses);
       if (getenv("POBK_K2_BANKSTATS")) {  // development aid: modelled wavefronts per x~ access
         double& acc_new = bank_stats[0]; double& acc_old = bank_stats[1]; double& acc_n = bank_stats[2];
         std::vector<std::vector<int>> members(ng);
@@ -2050,6 +2051,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
               bank_stats[0] / bank_stats[2], bank_stats[1] / bank_stats[2]);
   }
   const int np_max = std::max(1, *std::max_element(np_t.begin(), np_t.end()));
+  if (np_max > 65535) { why = "private columns per tile exceed the 16-bit interior column index"; return false; }
   const size_t base_smem = fixed + meta_bytes + 8 * (size_t)kR * ((size_t)np_max + 1);  // private x~ + the zero slot
   int NS = (int)std::min<size_t>(kMaxSlots, (kSmemTotal - base_smem) / kSlot);
   if (getenv("POBK_K2_NS_CAP")) NS = std::min(NS, atoi(getenv("POBK_K2_NS_CAP")));  // development experiments
@@ -2116,7 +2118,8 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
     const SliceLayout L(R, W, bnd, kR);
     double* val = (double*)blk;
     double* fv = (double*)(blk + L.o_f);
-    unsigned* col = (unsigned*)(blk + L.o_col);
+    unsigned* col = (unsigned*)(blk + L.o_col);             // boundary slices
+    unsigned short* col16 = (unsigned short*)(blk + L.o_col);  // interior slices
     unsigned* mout = (unsigned*)(blk + L.o_mout);
     unsigned short* len = (unsigned short*)(blk + L.o_len);
     for (int r = 0; r < R; r++) {
@@ -2124,11 +2127,15 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
       for (int j = 0; j < rlen(i); j++) {
         const int64_t q = At.ptr[i] + j;
         const int32_t cg = At.col[q];
-        col[j * R + r] = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
+        if (bnd) col[j * R + r] = shared[cg] ? (kShared | (unsigned)cg) : (unsigned)local[cg];
+        else col16[j * R + r] = (unsigned short)local[cg];
         val[j * R + r] = At.val[q];
         if (bnd) mout[j * R + r] = shared[cg] ? mout_of_entry[q] : 0u;
       }
-      for (int j = rlen(i); j < W; j++) col[j * R + r] = (unsigned)np_max;  // ELL padding: zero slot, value +0
+      for (int j = rlen(i); j < W; j++) {  // ELL padding: zero slot, value +0
+        if (bnd) col[j * R + r] = (unsigned)np_max;
+        else col16[j * R + r] = (unsigned short)np_max;
+      }
       if (bnd) ((double*)(blk + L.o_n2))[r] = nrm2[i];  // ||a~_i||^2 (row_sqnorms: the oracle's O1 order)
       len[r] = (unsigned short)rlen(i);
       for (int q = 0; q < kR; q++) fv[kR * r + q] = 0.0;  // f~ is scattered in per solve (k2_scatter_f)
@@ -2158,6 +2165,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
         const unsigned char* blk = stream.data() + slice_pos[si];
         const SliceLayout L(R, W, slice_bnd[si], kR);
         const unsigned* col = (const unsigned*)(blk + L.o_col);
+        const unsigned short* col16 = (const unsigned short*)(blk + L.o_col);
         const unsigned* mout = (const unsigned*)(blk + L.o_mout);
         const unsigned short* len = (const unsigned short*)(blk + L.o_len);
         for (int r = 0; r < R; r++) {
@@ -2165,7 +2173,7 @@ bool k2_build(Plan& p, const HostCSR& At, const std::vector<double>& nrm2, int t
           if (seen[i]++) return bad("row " + std::to_string(i) + " streamed twice");
           if (len[r] > W) return bad("row length > slice width");
           for (int j = 0; j < W; j++) {
-            const unsigned c = col[j * R + r];
+            const unsigned c = slice_bnd[si] ? col[j * R + r] : (unsigned)col16[j * R + r];
             if (c & kShared) {
               if ((c & kIdx) >= (unsigned)m || !slice_bnd[si]) return bad("shared column");
               const unsigned mo = mout[j * R + r] & ~kWrap;
