@@ -881,6 +881,66 @@ __device__ __forceinline__ void slice_interior2(const SliceAddr& S, int W, unsig
   }
 }
 
+// slice_interior2 with pass 1's operands parked in TMEM (slice_interior_tm's scheme; 28 columns
+// per 4-entry batch: the columns, the values and both right-hand sides' x~)
+__device__ __forceinline__ void slice_interior2_tm(const SliceAddr& S, int W, unsigned xb, unsigned act, unsigned taddr) {
+  static_assert(kIB == 4, "slice_interior2_tm parks 4-entry batches (28 TMEM columns each)");
+  double s0 = 0.0, s1 = 0.0, n2 = 0.0;
+  for (int jb = 0; jb < W; jb += kIB) {
+    unsigned c[kIB];
+    double av[kIB];
+    double2 xv[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) xv[u] = lds128(xb + 16u * c[u]);
+#pragma unroll
+    for (int u = 0; u < kIB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    const unsigned ta = taddr + (unsigned)(jb / kIB) * 28u;
+    tm_st4(ta, c[0], c[1], c[2], c[3]);
+    tm_st4(ta + 4, __double2loint(av[0]), __double2hiint(av[0]), __double2loint(av[1]), __double2hiint(av[1]));
+    tm_st4(ta + 8, __double2loint(av[2]), __double2hiint(av[2]), __double2loint(av[3]), __double2hiint(av[3]));
+#pragma unroll
+    for (int u = 0; u < kIB; u++)
+      tm_st4(ta + 12 + 4 * u, __double2loint(xv[u].x), __double2hiint(xv[u].x), __double2loint(xv[u].y), __double2hiint(xv[u].y));
+    double p0[kIB], p1[kIB], qq[kIB];
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const bool in = jb + u < W;
+      const double a = in ? av[u] : 0.0, x0 = in ? xv[u].x : 0.0, x1 = in ? xv[u].y : 0.0;
+      p0[u] = pin(__dmul_rn(a, x0));
+      p1[u] = pin(__dmul_rn(a, x1));
+      qq[u] = pin(__dmul_rn(a, a));
+    }
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      s0 = __dadd_rn(s0, p0[u]);
+      s1 = __dadd_rn(s1, p1[u]);
+      n2 = __dadd_rn(n2, qq[u]);
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  const double y2 = rcp_ahead(n2);  // (one reciprocal for both quotients)
+  const double al0 = div_by_rcp(__dsub_rn(S.f, s0), n2, y2), al1 = div_by_rcp(__dsub_rn(S.f1, s1), n2, y2);
+  for (int jb = 0; jb < W; jb += kIB) {
+    const unsigned ta = taddr + (unsigned)(jb / kIB) * 28u;
+    unsigned c[kIB], w[24];
+    tm_ld4(ta, c[0], c[1], c[2], c[3]);
+#pragma unroll
+    for (int q = 0; q < 6; q++) tm_ld4(ta + 4 + 4 * q, w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < kIB; u++) {
+      const double av = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]);
+      const double x0 = __hiloint2double((int)w[8 + 4 * u + 1], (int)w[8 + 4 * u]);
+      const double x1 = __hiloint2double((int)w[8 + 4 * u + 3], (int)w[8 + 4 * u + 2]);
+      const double y0 = (act & 1u) ? __dadd_rn(x0, __dmul_rn(al0, av)) : x0;
+      const double y1 = (act & 2u) ? __dadd_rn(x1, __dmul_rn(al1, av)) : x1;
+      sts128_if(jb + u < S.myl, xb + 16u * c[u], y0, y1);
+    }
+  }
+}
+
 // boundary slice of a two-RHS plan (BSlice's structure; a lane's mailbox words: entry j's pair at
 // mbox_in + 2j, so one 256-bit load polls two entries)
 struct BSliceR2 {
@@ -1037,9 +1097,9 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   constexpr int kPub = kNCW - 1;      // compute warp that runs the per-sweep grid decision
   // interior slices park pass 1's operands in TMEM for pass 2 (slice_interior_tm): each warp owns
   // a TMEM region of its lane quarter (warp % 4), 512 / (warps per quarter) columns wide
-  constexpr bool kTM = kR == 1 && POBK_K2_TMEM;
+  constexpr bool kTM = POBK_K2_TMEM;
   constexpr int kTmCols = 512 / ((kNT / 32 + 3) / 4);        // columns per warp region (256 / 128)
-  constexpr int kTmMaxW = (kTmCols / 20) * kIB;              // widest slice whose operands fit (20 columns per 4 entries)
+  constexpr int kTmMaxW = (kTmCols / (kR == 1 ? 20 : 28)) * kIB;  // widest slice whose operands fit (20 / 28 columns per 4 entries)
   extern __shared__ __align__(128) unsigned char smem[];
   const int NS = a.NS;
   unsigned char* ring = smem;                                // NS * kSlot
@@ -1237,7 +1297,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
               if (lane == 0) trp[10] = gtimer();
             }
           } else if constexpr (kR == 2) {
-            slice_interior2(S, W, xb, actm);
+            if (kTM && W <= kTmMaxW) slice_interior2_tm(S, W, xb, actm, tmem_w);
+            else slice_interior2(S, W, xb, actm);
           } else {
             if (kTM && W <= kTmMaxW) slice_interior_tm(S, W, xb, tmem_w);
             else slice_interior(S, W, xb);
