@@ -79,7 +79,10 @@ enum {
 typedef struct {
   double thr;        /* 0 (default): structural orthogonality (disjoint supports, Z5/Z7);
                         > 0: |cos(a_i, a_l)| < thr counts as orthogonal, categories
-                        may overlap and use the simultaneous (fp64 atomic) update */
+                        may overlap and use the simultaneous update: every alpha of the step
+                        at the same x, then per column x_c += alpha_i a_ic in ascending row
+                        order (the oracle's order: bitwise; environment POBK_THR_ATOMIC=1:
+                        fp64 atomics, order nondeterministic) -- K1/K3 only */
   int32_t reorder;   /* 1 (default): RCM; 0: identity (narrow-band matrices) */
   int32_t kernel;    /* POBK_KERNEL_*; default AUTO */
   int32_t tile_rows; /* K2 target rows per tile; 0 = auto */
