@@ -33,7 +33,7 @@
 //  * A task's boundary slices come first; their warps note the shared entries, poll the
 //    mailboxes, then read the private operands with the row sums; the interior slices run
 //    meanwhile on the other warps.
-//  * The tile's slices are packed, across task boundaries, into <= 16 KB chunks streamed by 1-D
+//  * The tile's slices are packed, across task boundaries, into <= 24 KB chunks streamed by 1-D
 //    TMA (cp.async.bulk, L2 evict-first) into a ring of NS slots by the PRODUCER warp (the last
 //    warp), which never touches x~.
 //  * Stop checks at the end of a due sweep.  RSE: each tile sums (x~ - x~*)^2
@@ -47,6 +47,10 @@
 //    continuing across tasks), so consecutive boundary slices run on different SM sub-partitions.
 //  * One kernel instantiation per plan shape (threads, vector-slice width, interior mode): all
 //    paths inlined into one kernel spilled registers and doubled the sweep time.
+//  * Tensor memory as a per-thread parking area (DESIGN.md §5.2 (vii)): an interior slice's
+//    pass 1 parks its columns, values and x~ in TMEM (tcgen05.st) and pass 2 reads them back
+//    (tcgen05.ld) instead of re-reading them from shared memory, whose pipe the interior slices
+//    saturate; interior slices store 16-bit column indices (tile-local).
 #include <cuda_runtime.h>
 
 #include <algorithm>
