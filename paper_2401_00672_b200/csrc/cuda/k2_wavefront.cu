@@ -103,6 +103,10 @@ constexpr int kRU = POBK_K2_RSEU;  // end-of-sweep RSE scan: loads in flight per
 #ifndef POBK_K2_TMEM
 #define POBK_K2_TMEM 1  // interior pass-2 operands in tensor memory (measured r02f: config 4 96.8 -> 93.7 us/sweep)
 #endif
+// interior slices parked in TMEM: 8-entry batches for slices wider than 12 (fewer dependent
+// load rounds: config 4 94.2 -> 92.6 us/sweep), 4-entry ones below (less clamped padding:
+// config 5's 9-entry rows -- 8-entry batches cost it 6%)
+constexpr int kTmWide = 12;
 #ifndef POBK_K2_IBATCH
 #define POBK_K2_IBATCH 4  // (measured r02: 4 vs 8 -- config 4 97.6 vs 98.1 us/sweep, config 5 200.6 vs 190.3 G)
 #endif
@@ -457,53 +461,59 @@ __device__ __forceinline__ void tm_ld4(unsigned a, unsigned& v0, unsigned& v1, u
                : "r"(a)
                : "memory");
 }
+template <int IB>
 __device__ __forceinline__ void slice_interior_tm(const SliceAddr& S, int W, unsigned xb, unsigned taddr) {
-  static_assert(kIB == 4, "slice_interior_tm parks 4-entry batches (20 TMEM columns each)");
+  static_assert(IB % 4 == 0, "batches park in 4-word TMEM stores");
+  // per batch: columns [IB words] | values [2 IB] | x~ [2 IB]
   double s = 0.0, n2 = 0.0;
-  for (int jb = 0; jb < W; jb += kIB) {
-    unsigned c[kIB];
-    double av[kIB], xv[kIB];
+  for (int jb = 0; jb < W; jb += IB) {
+    unsigned c[IB];
+    double av[IB], xv[IB];
 #pragma unroll
-    for (int u = 0; u < kIB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
+    for (int u = 0; u < IB; u++) c[u] = lds16(S.cb + min(jb + u, W - 1) * S.cs);
 #pragma unroll
-    for (int u = 0; u < kIB; u++) xv[u] = lds64(xb + 8u * c[u]);
+    for (int u = 0; u < IB; u++) xv[u] = lds64(xb + 8u * c[u]);
 #pragma unroll
-    for (int u = 0; u < kIB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
-    const unsigned ta = taddr + (unsigned)(jb / kIB) * 20u;
-    tm_st4(ta, c[0], c[1], c[2], c[3]);
-    tm_st4(ta + 4, __double2loint(av[0]), __double2hiint(av[0]), __double2loint(av[1]), __double2hiint(av[1]));
-    tm_st4(ta + 8, __double2loint(av[2]), __double2hiint(av[2]), __double2loint(av[3]), __double2hiint(av[3]));
-    tm_st4(ta + 12, __double2loint(xv[0]), __double2hiint(xv[0]), __double2loint(xv[1]), __double2hiint(xv[1]));
-    tm_st4(ta + 16, __double2loint(xv[2]), __double2hiint(xv[2]), __double2loint(xv[3]), __double2hiint(xv[3]));
-    double pp[kIB], qq[kIB];
+    for (int u = 0; u < IB; u++) av[u] = lds64(S.vb + min(jb + u, W - 1) * S.vs);
+    const unsigned ta = taddr + (unsigned)(jb / IB) * (5u * IB);
 #pragma unroll
-    for (int u = 0; u < kIB; u++) {
+    for (int g = 0; g < IB / 4; g++) tm_st4(ta + 4 * g, c[4 * g], c[4 * g + 1], c[4 * g + 2], c[4 * g + 3]);
+#pragma unroll
+    for (int g = 0; g < IB / 2; g++)
+      tm_st4(ta + IB + 4 * g, __double2loint(av[2 * g]), __double2hiint(av[2 * g]), __double2loint(av[2 * g + 1]),
+             __double2hiint(av[2 * g + 1]));
+#pragma unroll
+    for (int g = 0; g < IB / 2; g++)
+      tm_st4(ta + 3 * IB + 4 * g, __double2loint(xv[2 * g]), __double2hiint(xv[2 * g]), __double2loint(xv[2 * g + 1]),
+             __double2hiint(xv[2 * g + 1]));
+    double pp[IB], qq[IB];
+#pragma unroll
+    for (int u = 0; u < IB; u++) {
       const bool in = jb + u < W;
       const double a = in ? av[u] : 0.0, x = in ? xv[u] : 0.0;
       pp[u] = pin(__dmul_rn(a, x));
       qq[u] = pin(__dmul_rn(a, a));
     }
 #pragma unroll
-    for (int u = 0; u < kIB; u++) {
+    for (int u = 0; u < IB; u++) {
       s = __dadd_rn(s, pp[u]);
       n2 = __dadd_rn(n2, qq[u]);
     }
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   const double alpha = __ddiv_rn(__dsub_rn(S.f, s), n2);
-  for (int jb = 0; jb < W; jb += kIB) {
-    const unsigned ta = taddr + (unsigned)(jb / kIB) * 20u;
-    unsigned c[kIB], w[16];
-    tm_ld4(ta, c[0], c[1], c[2], c[3]);
-    tm_ld4(ta + 4, w[0], w[1], w[2], w[3]);
-    tm_ld4(ta + 8, w[4], w[5], w[6], w[7]);
-    tm_ld4(ta + 12, w[8], w[9], w[10], w[11]);
-    tm_ld4(ta + 16, w[12], w[13], w[14], w[15]);
+  for (int jb = 0; jb < W; jb += IB) {
+    const unsigned ta = taddr + (unsigned)(jb / IB) * (5u * IB);
+    unsigned c[IB], w[4 * IB];
+#pragma unroll
+    for (int g = 0; g < IB / 4; g++) tm_ld4(ta + 4 * g, c[4 * g], c[4 * g + 1], c[4 * g + 2], c[4 * g + 3]);
+#pragma unroll
+    for (int g = 0; g < IB; g++) tm_ld4(ta + IB + 4 * g, w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int u = 0; u < kIB; u++) {
+    for (int u = 0; u < IB; u++) {
       const double av = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]);
-      const double xv = __hiloint2double((int)w[8 + 2 * u + 1], (int)w[8 + 2 * u]);
+      const double xv = __hiloint2double((int)w[2 * IB + 2 * u + 1], (int)w[2 * IB + 2 * u]);
       sts64_if(jb + u < S.myl, xb + 8u * c[u], __dadd_rn(xv, __dmul_rn(alpha, av)));
     }
   }
@@ -1103,7 +1113,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
   // a TMEM region of its lane quarter (warp % 4), 512 / (warps per quarter) columns wide
   constexpr bool kTM = POBK_K2_TMEM;
   constexpr int kTmCols = 512 / ((kNT / 32 + 3) / 4);        // columns per warp region (256 / 128)
-  constexpr int kTmMaxW = (kTmCols / (kR == 1 ? 20 : 28)) * kIB;  // widest slice whose operands fit (20 / 28 columns per 4 entries)
+  constexpr int kTmMaxW = kR == 1 ? (kTmCols / 20) * 4 : (kTmCols / 28) * kIB;  // widest slice whose operands fit
+  constexpr int kTmMaxW8 = (kTmCols / 40) * 8;                                    // (8-entry batches)
   extern __shared__ __align__(128) unsigned char smem[];
   const int NS = a.NS;
   unsigned char* ring = smem;                                // NS * kSlot
@@ -1304,7 +1315,8 @@ __global__ void __launch_bounds__(kNT, 1) k2_sweeps(K2Args a) {
             if (kTM && W <= kTmMaxW) slice_interior2_tm(S, W, xb, actm, tmem_w);
             else slice_interior2(S, W, xb, actm);
           } else {
-            if (kTM && W <= kTmMaxW) slice_interior_tm(S, W, xb, tmem_w);
+            if (kTM && kNT == 256 && W > kTmWide && W <= kTmMaxW8) slice_interior_tm<8>(S, W, xb, tmem_w);
+            else if (kTM && W <= kTmMaxW) slice_interior_tm<4>(S, W, xb, tmem_w);
             else slice_interior(S, W, xb);
           }
           __syncwarp();
