@@ -77,14 +77,16 @@ cudaError_t capture_sweep(Plan& p, cudaStream_t cs, long long& nodes) {
       nodes++;
     } else {
       k1_alpha<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, p.d_alpha, s0, s1);
+      nodes++;
+      const int c0 = p.h_ov_colptr[k], c1 = p.h_ov_colptr[k + 1];
       if (atomic) {
         k1_scatter_atomic<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_alpha, p.d_xt, s0, s1);
-      } else {
-        const int c0 = p.h_ov_colptr[k], c1 = p.h_ov_colptr[k + 1];
+        nodes++;
+      } else if (c1 > c0) {
         k1_scatter_ordered<<<(c1 - c0 + kNT - 1) / kNT, kNT, 0, cs>>>(p.ov_cols, p.ov_eptr, p.ov_es, p.ov_ev, p.d_alpha,
                                                                      p.d_xt, c0, c1);
+        nodes++;
       }
-      nodes += 2;
     }
   }
   return cudaGetLastError();
