@@ -12,7 +12,8 @@ Tolerance 1e-1 (1e-6 is unreachable within the paper's 5e5-swe
 config at row granularity; the protocol fixes 1e-1 for configs 3-5).
 
   value      = sum over ranks of nnz x sweeps / max-over-ranks device time of the K steps
-  e2e        = the same metric through pobk_solve_host (pinned host f, x0, x*; H2D + D2H inside)
+  e2e        = the same metric through pobk_solve_host (pinned host f, x0, x*; H2D + D2H inside);
+               batched configs through pobk_solve_batch_host (copies overlapped with other systems' sweeps)
   roofline   = the sweep kernel: algorithmic bytes B = 12 nnz + 12 m per sweep
                x sweeps / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline = the oracle (plain C, 1 core) on a bounded sample of the same workload
@@ -262,23 +263,15 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if len(plans) > 1:
-        # batched systems: the step's pinned host inputs -> device (copies on the stream), one
-        # pobk_solve_batch call, the solutions -> pinned host; all inside the timed region
-        tf = [torch.from_numpy(v) for v in hf]
-        txs = [torch.from_numpy(v) for v in hxs]
+        # batched systems: one pobk_solve_batch_host call per step on the pinned host vectors (its
+        # internal copy streams move the other systems' inputs in and the finished solutions out
+        # while systems solve on the lanes); all inside the timed region
         for st in range(a.steps):
-            hxt = [torch.from_numpy(v) for v in hx[st if per_step else 0]]
+            hxs_t = hx[st if per_step else 0]
             if not per_step:
-                for v in hxt:
-                    v.zero_()
-            for j in range(len(plans)):
-                fs[j].copy_(tf[j], non_blocking=True)
-                xs[j].copy_(hxt[j], non_blocking=True)
-                xss[j].copy_(txs[j], non_blocking=True)
-            e2e_reps.extend(pk.solve_batch(plans, fs, xs, xss, tol=tol, max_sweeps=500000, stop="rse"))
-            for j in range(len(plans)):
-                hxt[j].copy_(xs[j], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+                for v in hxs_t:
+                    v[:] = 0.0
+            e2e_reps.extend(pk.solve_batch_host(plans, hf, hxs_t, hxs, tol=tol, max_sweeps=500000, stop="rse"))
     else:
         for st in range(a.steps):
             for p, f, x, xst in zip(plans, hf, hx[st if per_step else 0], hxs):

@@ -200,6 +200,18 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
                              const double* const* xstar_dev, const pobk_solve_opts* opts, void* stream,
                              pobk_report* reps);
 
+/* pobk_solve_batch with HOST vectors (the batched end-to-end path): arrays of nb host pointers
+ * (f, x0 in / solution out, x* for POBK_STOP_RSE), same systems, stop rules, reports and results
+ * as pobk_solve_batch.  On concurrent lanes the host->device copies of later systems and the
+ * device->host copies of finished ones run on internal copy streams while other systems solve,
+ * so only the first round's inputs and the last round's solutions are not overlapped with
+ * sweeps; otherwise each system goes through pobk_solve_host back to back.  Each plan keeps a 3m
+ * staging buffer on the device.  Host buffers may be pageable; the overlap needs pinned memory.
+ * Ordered after prior work on `stream`; blocks until reps are filled and x holds the solutions. */
+pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,
+                                  const double* const* xstar, const pobk_solve_opts* opts, void* stream,
+                                  pobk_report* reps);
+
 /* *out = ||f - A x||_2 in the user frame (fused SpMV + squared-norm kernel, deterministic
  * two-level reduction): the residual of Ax = f whose ratio to ||f|| is the RELRES stop
  * (SURVEY Z13), the paper's RSE needing x*.  Device vectors; result returned to the host. */

@@ -14,7 +14,7 @@ import numpy as np
 from . import _lib as L
 from ._lib import PobkError, Report, KERNEL, STOP, TERM_NAME  # noqa: F401
 
-__all__ = ["Plan", "PobkError", "Report", "solve_batch", "lane_tile_rows", "half_gpu_tile_rows", "KERNEL", "STOP"]
+__all__ = ["Plan", "PobkError", "Report", "solve_batch", "solve_batch_host", "lane_tile_rows", "half_gpu_tile_rows", "KERNEL", "STOP"]
 
 
 def _torch():
@@ -228,6 +228,28 @@ def solve_batch(plans, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int 
     L.check(L.lib.pobk_solve_batch(H, nb, ctypes.cast(F, ctypes.c_void_p), ctypes.cast(X, ctypes.c_void_p),
                                    ctypes.cast(XS, ctypes.c_void_p) if XS is not None else None, ctypes.byref(o),
                                    _stream(stream), ctypes.cast(reps, ctypes.c_void_p)))
+    return list(reps)
+
+
+def solve_batch_host(plans, fs, xs, x_stars=None, tol: float = 1e-6, max_sweeps: int = 500000, stop="rse",
+                     check_every: int = 1, stream=None) -> list[Report]:
+    """pobk_solve_batch_host: solve_batch with host (numpy float64) vectors; xs are updated in
+    place.  On concurrent lanes the copies of other systems overlap the sweeps (pinned memory)."""
+    nb = len(plans)
+    for j, (p, f, x) in enumerate(zip(plans, fs, xs)):
+        for name, a in (("f", f), ("x", x), ("x_star", x_stars[j] if x_stars else None)):
+            if a is not None and (not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous
+                                  or a.size != p.m):
+                raise TypeError(f"system {j}: {name} must be a contiguous float64 numpy array of length {p.m}")
+    H = (ctypes.c_void_p * nb)(*[p._h.value for p in plans])
+    F = (ctypes.c_void_p * nb)(*[L.ptr(f).value for f in fs])
+    X = (ctypes.c_void_p * nb)(*[L.ptr(x).value for x in xs])
+    XS = (ctypes.c_void_p * nb)(*[L.ptr(x).value for x in x_stars]) if x_stars else None
+    reps = (L.Report * nb)()
+    o = _solve_opts(tol, max_sweeps, stop, check_every)
+    L.check(L.lib.pobk_solve_batch_host(H, nb, ctypes.cast(F, ctypes.c_void_p), ctypes.cast(X, ctypes.c_void_p),
+                                        ctypes.cast(XS, ctypes.c_void_p) if XS is not None else None, ctypes.byref(o),
+                                        _stream(stream), ctypes.cast(reps, ctypes.c_void_p)))
     return list(reps)
 
 

@@ -84,6 +84,7 @@ SIGNATURES = {
     "pobk_solve": (I32, [P, P, P, P, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report)]),
     "pobk_solve_host": (I32, [P, P, P, P, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report)]),
     "pobk_solve_batch": (I32, [ctypes.POINTER(P), I32, P, P, P, ctypes.POINTER(SolveOpts), P, P]),
+    "pobk_solve_batch_host": (I32, [ctypes.POINTER(P), I32, P, P, P, ctypes.POINTER(SolveOpts), P, P]),
     "pobk_solve_multi": (I32, [P, I32, P, P, P, ctypes.POINTER(SolveOpts), P, P]),
     "pobk_residual_norm": (I32, [P, P, P, P, ctypes.POINTER(F64)]),
     "pobk_residual_sumsq_rows": (I32, [P, I64, I64, P, P, P, ctypes.POINTER(F64)]),

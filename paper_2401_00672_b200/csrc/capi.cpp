@@ -554,25 +554,16 @@ pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const 
   return POBK_OK;
 }
 
-pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,
-                             const double* const* xstar, const pobk_solve_opts* opts, void* stream, pobk_report* reps) {
-  g_err.clear();
-  if (nb < 0 || (nb > 0 && (!plans || !f || !x))) return fail(POBK_ERR_ARG, "bad batch arguments");
-  // Lanes: when every system is a K2 plan on the same device and nl >= 2 of their grids fit side
-  // by side (e.g. plans built with half-GPU tiles), system b runs on internal stream b mod nl, so
-  // nl cooperative sweep kernels share the GPU (each system's latency-bound step chain overlaps
-  // the others').  Results are those of back-to-back solves (tiling never changes them).
-  // every system's arguments are checked before anything is enqueued
-  std::vector<pobk_solve_opts> os(nb);
-  for (int32_t b = 0; b < nb; b++) {
-    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
-    if (st != POBK_OK) {
-      g_err = "system " + std::to_string(b) + ": " + g_err;
-      return st;
-    }
-  }
+// The lanes rule of pobk_solve_batch / pobk_solve_batch_host: when every system is a K2 plan on
+// the same device, no plan is named twice, and nl >= 2 of their grids fit side by side (e.g. plans
+// built with half-GPU tiles), system b runs on internal stream b mod nl, so nl cooperative sweep
+// kernels share the GPU (each system's latency-bound step chain overlaps the others').  Returns
+// nl (>= 2), or 1 for back-to-back solves.  Results are those of back-to-back solves (tiling
+// never changes them).
+static int batch_lane_count(pobk_plan_t* plans, int32_t nb, int& dev) {
   bool lanes = nb >= 2;
-  int sms = 148, dev = -1;
+  int sms = 148;
+  dev = -1;
   for (int32_t b = 0; b < nb && lanes; b++) {
     if (!plans[b] || plans[b]->device < 0 || plans[b]->kernel != POBK_KERNEL_WAVEFRONT || !plans[b]->k2) lanes = false;
     else if (dev >= 0 && plans[b]->device != dev) lanes = false;
@@ -583,16 +574,54 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
   for (int32_t b = 0; b < nb && lanes; b++)
     for (int32_t c = 0; c < b && lanes; c++)
       if (plans[c] == plans[b]) lanes = false;
-  int nl = 1;  // lanes: as many K2 grids as fit side by side (at most 4)
-  if (lanes) {
-    int v = 0;  // (cudaGetDeviceProperties costs milliseconds; the attribute query does not)
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
-    int tmax = 1;
-    for (int32_t b = 0; b < nb; b++) tmax = std::max(tmax, (int)plans[b]->ntiles);
-    nl = std::min({4, sms / tmax, (int)nb});
-    lanes = nl >= 2 && !getenv("POBK_BATCH_SERIAL");
+  if (!lanes) return 1;
+  int v = 0;  // (cudaGetDeviceProperties costs milliseconds; the attribute query does not)
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  int tmax = 1;
+  for (int32_t b = 0; b < nb; b++) tmax = std::max(tmax, (int)plans[b]->ntiles);
+  const int nl = std::min({4, sms / tmax, (int)nb});
+  return nl >= 2 && !getenv("POBK_BATCH_SERIAL") ? nl : 1;
+}
+
+// internal streams of the batch calls (per host thread and device; created once): the lanes, and
+// the host->device / device->host copy streams of pobk_solve_batch_host
+struct LaneSet {
+  cudaStream_t lane[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+static cudaError_t lane_set(int dev, LaneSet** out) {
+  static thread_local int lane_dev = -1;
+  static thread_local LaneSet set;
+  if (lane_dev != dev) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < 4 && e == cudaSuccess; i++) e = cudaStreamCreateWithFlags(&set.lane[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&set.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&set.d2h, cudaStreamNonBlocking);
+    for (int i = 0; i < 5 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&set.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    lane_dev = dev;
   }
-  if (!lanes) {
+  *out = &set;
+  return cudaSuccess;
+}
+
+pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,
+                             const double* const* xstar, const pobk_solve_opts* opts, void* stream, pobk_report* reps) {
+  g_err.clear();
+  if (nb < 0 || (nb > 0 && (!plans || !f || !x))) return fail(POBK_ERR_ARG, "bad batch arguments");
+  // every system's arguments are checked before anything is enqueued (lanes: batch_lane_count)
+  std::vector<pobk_solve_opts> os(nb);
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
+    if (st != POBK_OK) {
+      g_err = "system " + std::to_string(b) + ": " + g_err;
+      return st;
+    }
+  }
+  int dev = -1;
+  const int nl = batch_lane_count(plans, nb, dev);
+  if (nl < 2) {
     for (int32_t b = 0; b < nb; b++) {
       pobk_status st = pobk_solve(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
       if (st != POBK_OK) {
@@ -604,14 +633,10 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
   }
   DeviceGuard g(dev);
   if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
-  static thread_local int lane_dev = -1;
-  static thread_local cudaStream_t lane_s[4] = {nullptr, nullptr, nullptr, nullptr};
-  static thread_local cudaEvent_t lane_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  if (lane_dev != dev) {  // (per thread and device; created once)
-    for (int i = 0; i < 4; i++) CUDA_TRY(cudaStreamCreateWithFlags(&lane_s[i], cudaStreamNonBlocking));
-    for (int i = 0; i < 5; i++) CUDA_TRY(cudaEventCreateWithFlags(&lane_ev[i], cudaEventDisableTiming));
-    lane_dev = dev;
-  }
+  LaneSet* ls = nullptr;
+  CUDA_TRY(lane_set(dev, &ls));
+  cudaStream_t* lane_s = ls->lane;
+  cudaEvent_t* lane_ev = ls->ev;
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaEventRecord(lane_ev[4], s));
   for (int i = 0; i < nl; i++) CUDA_TRY(cudaStreamWaitEvent(lane_s[i], lane_ev[4], 0));
@@ -633,6 +658,113 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
     g_err = keep;
     return enq;
   }
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = solve_finish(*plans[b], os[b], reps ? reps + b : nullptr);
+    if (st != POBK_OK) return st;
+  }
+  return POBK_OK;
+}
+
+pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,
+                                  const double* const* xstar, const pobk_solve_opts* opts, void* stream,
+                                  pobk_report* reps) {
+  g_err.clear();
+  if (nb < 0 || (nb > 0 && (!plans || !f || !x))) return fail(POBK_ERR_ARG, "bad batch arguments");
+  std::vector<pobk_solve_opts> os(nb);
+  for (int32_t b = 0; b < nb; b++) {
+    pobk_status st = check_solve_args(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, os[b], opts);
+    if (st != POBK_OK) {
+      g_err = "system " + std::to_string(b) + ": " + g_err;
+      return st;
+    }
+  }
+  int dev = -1;
+  const int nl = batch_lane_count(plans, nb, dev);
+  if (nl < 2) {  // back to back: each system through pobk_solve_host (copies, solve, copy back)
+    for (int32_t b = 0; b < nb; b++) {
+      pobk_status st = pobk_solve_host(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
+      if (st != POBK_OK) {
+        g_err = "system " + std::to_string(b) + ": " + g_err;
+        return st;
+      }
+    }
+    return POBK_OK;
+  }
+  DeviceGuard g(dev);
+  if (!g.ok) return fail(POBK_ERR_CUDA, "cudaSetDevice failed");
+  LaneSet* ls = nullptr;
+  CUDA_TRY(lane_set(dev, &ls));
+  // the plans' staging vectors (f, x, x*), allocated before anything is enqueued
+  for (int32_t b = 0; b < nb; b++)
+    if (!plans[b]->d_io) {
+      DeviceGuard gb(plans[b]->device);
+      CUDA_TRY(dalloc(*plans[b], &plans[b]->d_io, 3 * plans[b]->m));
+    }
+  // per system: inputs arrived (h2d stream -> its lane), solve done (lane -> d2h stream)
+  std::vector<cudaEvent_t> ev(2 * (size_t)nb, nullptr);
+  auto destroy = [&]() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  for (auto& e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      destroy();
+      return fail(POBK_ERR_CUDA, "cudaEventCreate failed");
+    }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t* lane_s = ls->lane;
+  pobk_status enq = POBK_OK;
+  cudaError_t ce = cudaEventRecord(ls->ev[4], s);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ls->h2d, ls->ev[4], 0);
+  for (int i = 0; i < nl && ce == cudaSuccess; i++) ce = cudaStreamWaitEvent(lane_s[i], ls->ev[4], 0);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ls->d2h, ls->ev[4], 0);
+  if (ce != cudaSuccess) {
+    destroy();
+    return fail(POBK_ERR_CUDA, cudaGetErrorString(ce));
+  }
+  // Every system's inputs go in on one copy stream in system order while earlier systems solve on
+  // their lanes; each solution comes back on the other copy stream as soon as its solve is done.
+  // So only the first round's inputs and the last round's outputs are not hidden behind sweeps.
+  for (int32_t b = 0; b < nb && enq == POBK_OK; b++) {
+    Plan& p = *plans[b];
+    const size_t bytes = p.m * sizeof(double);
+    double *df = p.d_io, *dx = p.d_io + p.m, *dxs = p.d_io + 2 * p.m;
+    const bool rse = os[b].stop == POBK_STOP_RSE;
+    cudaStream_t ln = lane_s[b % nl];
+    ce = cudaMemcpyAsync(df, f[b], bytes, cudaMemcpyHostToDevice, ls->h2d);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(dx, x[b], bytes, cudaMemcpyHostToDevice, ls->h2d);
+    if (ce == cudaSuccess && rse) ce = cudaMemcpyAsync(dxs, xstar[b], bytes, cudaMemcpyHostToDevice, ls->h2d);
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * b], ls->h2d);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ln, ev[2 * b], 0);
+    if (ce != cudaSuccess) {
+      enq = fail(POBK_ERR_CUDA, cudaGetErrorString(ce));
+      break;
+    }
+    enq = solve_device(p, df, dx, rse ? dxs : nullptr, os[b], ln, nullptr, true);
+    if (enq != POBK_OK) break;
+    ce = cudaEventRecord(ev[2 * b + 1], ln);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ls->d2h, ev[2 * b + 1], 0);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(x[b], dx, bytes, cudaMemcpyDeviceToHost, ls->d2h);
+    if (ce != cudaSuccess) enq = fail(POBK_ERR_CUDA, cudaGetErrorString(ce));
+  }
+  if (enq != POBK_OK) g_err = "batch: " + g_err;
+  // (also after a failed enqueue: `stream` is ordered after everything already enqueued and the
+  // internal streams are drained, so no copy or solve of this call outlives it)
+  const std::string keep = g_err;
+  ce = cudaSuccess;
+  cudaStream_t all[6] = {ls->h2d, ls->d2h, lane_s[0], lane_s[1], lane_s[2], lane_s[3]};
+  for (int i = 0; i < 2 + nl; i++) {
+    cudaError_t e1 = cudaEventRecord(ls->ev[i < 4 ? i : 3], all[i]);
+    if (e1 == cudaSuccess) e1 = cudaStreamWaitEvent(s, ls->ev[i < 4 ? i : 3], 0);
+    cudaError_t e2 = cudaStreamSynchronize(all[i]);
+    if (ce == cudaSuccess) ce = e1 != cudaSuccess ? e1 : e2;
+  }
+  destroy();
+  if (enq != POBK_OK) {
+    g_err = keep;
+    return enq;
+  }
+  if (ce != cudaSuccess) return fail(POBK_ERR_CUDA, cudaGetErrorString(ce));
   for (int32_t b = 0; b < nb; b++) {
     pobk_status st = solve_finish(*plans[b], os[b], reps ? reps + b : nullptr);
     if (st != POBK_OK) return st;

@@ -529,6 +529,46 @@ def test_batch_duplicate_plan_and_bad_args(env):
     assert not x0[0].any().item()
 
 
+@pytest.mark.parametrize("nb,lanes", [(5, True), (3, False)])
+def test_batch_host_equals_device_batch(env, nb, lanes):
+    """pobk_solve_batch_host (host vectors; copies of other systems overlapped with the sweeps on
+    concurrent lanes): every system's stop sweep, final RSE and solution are bitwise those of
+    pobk_solve_batch on device vectors, on lanes (half-GPU K2 tilings, odd batch) and back to back
+    (AUTO plans); pinned and pageable host buffers; a bad argument fails before anything runs."""
+    pk, torch = env
+    systems = [gen.make("batch9pt_1024", b, n=160) for b in range(nb)]
+    kw = dict(kernel="wavefront", tile_rows=pk.half_gpu_tile_rows(systems[0].m)) if lanes else {}
+    plans = [pk.Plan.from_system(s, **kw) for s in systems]
+    xs = [_dev(torch, np.zeros(s.m)) for s in systems]
+    reps = pk.solve_batch(plans, [_dev(torch, s.f) for s in systems], xs, [_dev(torch, s.x_star) for s in systems],
+                          tol=0.2)
+    for pinned in (True, False):
+        conv = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()) if pinned else np.ascontiguousarray
+        hf = [conv(s.f) for s in systems]
+        hxs = [conv(s.x_star) for s in systems]
+        hx = [conv(np.zeros(s.m)) for s in systems]
+        hreps = pk.solve_batch_host(plans, hf, hx, hxs, tol=0.2)
+        for r, hr, xd, xh in zip(reps, hreps, xs, hx):
+            assert hr.sweeps == r.sweeps and hr.final_value == r.final_value
+            assert np.array_equal(xh, xd.cpu().numpy())
+    s0 = systems[0]
+    pre = O.preprocess(s0.m, s0.indptr, s0.indices, s0.data)
+    assert np.array_equal(hx[0], O.run_sweeps(pre, s0.f, reps[0].sweeps))
+    bad = [np.zeros(s.m) for s in systems]
+    with pytest.raises(pk.PobkError):  # last system: RSE stop without x*
+        import ctypes
+        L = pk._lib
+        H = (ctypes.c_void_p * nb)(*[p._h.value for p in plans])
+        F = (ctypes.c_void_p * nb)(*[L.ptr(f).value for f in hf])
+        X = (ctypes.c_void_p * nb)(*[L.ptr(x).value for x in bad])
+        XS = (ctypes.c_void_p * nb)(*([L.ptr(x).value for x in hxs[:-1]] + [None]))
+        o = pk._solve_opts(0.2, 100, "rse", 1)
+        L.check(L.lib.pobk_solve_batch_host(H, nb, ctypes.cast(F, ctypes.c_void_p), ctypes.cast(X, ctypes.c_void_p),
+                                            ctypes.cast(XS, ctypes.c_void_p), ctypes.byref(o), None,
+                                            ctypes.cast((L.Report * nb)(), ctypes.c_void_p)))
+    assert not any(b.any() for b in bad)
+
+
 # ---------------------------------------------------------------- several right-hand sides (NEXT-3)
 @pytest.mark.parametrize("name,n,R,tol", [("lap3d7_64", 24, 3, 0.1), ("lap2d5_32", None, 8, 1e-3),
                                           ("geoknn_1m", 30000, 4, 0.1)])
