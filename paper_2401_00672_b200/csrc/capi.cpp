@@ -547,11 +547,15 @@ pobk_status pobk_solve_host(pobk_plan_t plan, const double* f, double* x, const 
   CUDA_TRY(cudaMemcpyAsync(df, f, bytes, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
   if (rse) CUDA_TRY(cudaMemcpyAsync(dxs, xstar, bytes, cudaMemcpyHostToDevice, s));
-  st = solve_device(p, df, dx, rse ? dxs : nullptr, o, s, rep);
-  if (st != POBK_OK) return st;
+  // the solution's copy back is enqueued behind the solve: one host synchronisation per call
+  st = solve_device(p, df, dx, rse ? dxs : nullptr, o, s, nullptr, true);
+  if (st != POBK_OK) {
+    (void)cudaStreamSynchronize(s);  // (nothing of this call outlives it)
+    return st;
+  }
   CUDA_TRY(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  return POBK_OK;
+  return solve_finish(p, o, rep);
 }
 
 // The lanes rule of pobk_solve_batch / pobk_solve_batch_host: when every system is a K2 plan on
