@@ -202,10 +202,11 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
 
 /* pobk_solve_batch with HOST vectors (the batched end-to-end path): arrays of nb host pointers
  * (f, x0 in / solution out, x* for POBK_STOP_RSE), same systems, stop rules, reports and results
- * as pobk_solve_batch.  On concurrent lanes the host->device copies of later systems and the
- * device->host copies of finished ones run on internal copy streams while other systems solve,
- * so only the first round's inputs and the last round's solutions are not overlapped with
- * sweeps; otherwise each system goes through pobk_solve_host back to back.  Each plan keeps a 3m
+ * as pobk_solve_batch.  With distinct plans on one device, the host->device copies of later
+ * systems and the device->host copies of finished ones run on internal copy streams while other
+ * systems solve (on concurrent lanes when pobk_solve_batch would use them, else on one internal
+ * stream), so only the first inputs and the last solutions are not overlapped with sweeps; a
+ * batch naming a plan twice goes through pobk_solve_host back to back.  Each plan keeps a 3m
  * staging buffer on the device.  Host buffers may be pageable; the overlap needs pinned memory.
  * Ordered after prior work on `stream`; blocks until reps are filled and x holds the solutions. */
 pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,

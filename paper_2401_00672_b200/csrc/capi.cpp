@@ -683,8 +683,20 @@ pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* 
     }
   }
   int dev = -1;
-  const int nl = batch_lane_count(plans, nb, dev);
-  if (nl < 2) {  // back to back: each system through pobk_solve_host (copies, solve, copy back)
+  int nl = batch_lane_count(plans, nb, dev);
+  if (nl < 2 && nb >= 2) {
+    // distinct plans on one device that do not fit side by side: one lane, the copies of the
+    // other systems still overlapped with each solve
+    bool ok = plans[0] && plans[0]->device >= 0;
+    dev = ok ? plans[0]->device : -1;
+    for (int32_t b = 1; b < nb && ok; b++) {
+      ok = plans[b] && plans[b]->device == dev;
+      for (int32_t c = 0; c < b && ok; c++) ok = plans[c] != plans[b];
+    }
+    nl = ok ? 1 : 0;
+  }
+  if (nb < 2) nl = 0;
+  if (nl < 1) {  // back to back: each system through pobk_solve_host (copies, solve, copy back)
     for (int32_t b = 0; b < nb; b++) {
       pobk_status st = pobk_solve_host(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);
       if (st != POBK_OK) {

@@ -533,8 +533,9 @@ def test_batch_duplicate_plan_and_bad_args(env):
 def test_batch_host_equals_device_batch(env, nb, lanes):
     """pobk_solve_batch_host (host vectors; copies of other systems overlapped with the sweeps on
     concurrent lanes): every system's stop sweep, final RSE and solution are bitwise those of
-    pobk_solve_batch on device vectors, on lanes (half-GPU K2 tilings, odd batch) and back to back
-    (AUTO plans); pinned and pageable host buffers; a bad argument fails before anything runs."""
+    pobk_solve_batch on device vectors, on lanes (half-GPU K2 tilings, odd batch) and on one
+    internal stream (AUTO plans); pinned and pageable host buffers; a bad argument fails before
+    anything runs; a plan named twice runs back to back."""
     pk, torch = env
     systems = [gen.make("batch9pt_1024", b, n=160) for b in range(nb)]
     kw = dict(kernel="wavefront", tile_rows=pk.half_gpu_tile_rows(systems[0].m)) if lanes else {}
@@ -567,6 +568,11 @@ def test_batch_host_equals_device_batch(env, nb, lanes):
                                             ctypes.cast(XS, ctypes.c_void_p), ctypes.byref(o), None,
                                             ctypes.cast((L.Report * nb)(), ctypes.c_void_p)))
     assert not any(b.any() for b in bad)
+    # a plan named twice: back to back through pobk_solve_host, each system its own result
+    hx2 = [np.zeros(systems[0].m) for _ in range(2)]
+    r2 = pk.solve_batch_host([plans[0], plans[0]], [hf[0], hf[0]], hx2, [hxs[0], hxs[0]], tol=0.2)
+    assert all(r.sweeps == reps[0].sweeps for r in r2)
+    assert np.array_equal(hx2[0], xs[0].cpu().numpy()) and np.array_equal(hx2[1], xs[0].cpu().numpy())
 
 
 # ---------------------------------------------------------------- several right-hand sides (NEXT-3)
