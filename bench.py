@@ -328,7 +328,8 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            tj = json.load(open(tp))
+            tj = json.load(open(tp))  # {workload: {kernel, dram_bytes_per_sweep, source}}
+            tj = tj.get(s0.name, {}) if "workload" not in tj else tj
             if tj.get("workload") == s0.name and tj.get("kernel") == all_reps[0].as_dict()["kernel"]:
                 traffic = tj.get("dram_bytes_per_sweep")
         except Exception:

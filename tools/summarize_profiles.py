@@ -1,6 +1,7 @@
 """Summarise ncu outputs from gpurun_out/ into committed profiles/ files.
 
-    python tools/summarize_profiles.py <round-tag> <launches.csv> <full.ncu-rep> <sweeps-in-capture> <workload>
+    python tools/summarize_profiles.py <round-tag> <launches.csv | -> <full.ncu-rep> <sweeps-in-capture> <workload>
+profiles/traffic.json keeps one entry per workload (the bench's roofline `traffic`).
 """
 import csv
 import json
@@ -10,7 +11,7 @@ from collections import defaultdict
 
 tag, launches, rep, sweeps, workload = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), sys.argv[5]
 
-rows = [r for r in csv.reader(open(launches)) if len(r) > 14 and r[0] not in ("ID",)]
+rows = [r for r in csv.reader(open(launches)) if len(r) > 14 and r[0] not in ("ID",)] if launches != "-" else []
 by = defaultdict(lambda: [0, 0.0])
 for r in rows:
     name = r[4].replace("<unnamed>::", "").replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0].split("<")[0].strip()
@@ -23,7 +24,8 @@ out = [f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-con
        "| kernel | launches | total us | share |", "|---|---:|---:|---:|"]
 for k, (n, us) in sorted(by.items(), key=lambda kv: -kv[1][1]):
     out.append(f"| `{k}` | {n} | {us:.1f} | {100 * us / tot:.1f}% |")
-open(f"profiles/{tag}_launches.md", "w").write("\n".join(out) + "\n")
+if rows:
+    open(f"profiles/{tag}_launches.md", "w").write("\n".join(out) + "\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
@@ -49,6 +51,13 @@ for k in want:
         lines.append(f"| {k} | {m[k][1]} | {m[k][0]} |")
 lines += ["", f"DRAM bytes per sweep (read+write) = {(dr + dw) / sweeps / 1e6:.1f} MB"]
 open(f"profiles/{tag}_top_kernel_ncu.md", "w").write("\n".join(lines) + "\n")
-json.dump({"workload": workload, "kernel": "wavefront", "dram_bytes_per_sweep": (dr + dw) / sweeps,
-           "source": f"profiles/{tag}_top_kernel_ncu.md"}, open("profiles/traffic.json", "w"), indent=1)
-print("\n".join(out)); print("\n".join(lines))
+try:
+    tj = json.load(open("profiles/traffic.json"))
+    if "workload" in tj:  # (the one-entry format of earlier rounds)
+        tj = {tj["workload"]: tj}
+except Exception:
+    tj = {}
+tj[workload] = {"workload": workload, "kernel": "wavefront", "dram_bytes_per_sweep": (dr + dw) / sweeps,
+                "source": f"profiles/{tag}_top_kernel_ncu.md"}
+json.dump(tj, open("profiles/traffic.json", "w"), indent=1)
+print("\n".join(out if rows else [])); print("\n".join(lines))
