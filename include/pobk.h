@@ -206,7 +206,8 @@ pobk_status pobk_solve_batch(pobk_plan_t* plans, int32_t nb, const double* const
  * systems and the device->host copies of finished ones run on internal copy streams while other
  * systems solve (on concurrent lanes when pobk_solve_batch would use them, else on one internal
  * stream), so only the first inputs and the last solutions are not overlapped with sweeps; a
- * batch naming a plan twice goes through pobk_solve_host back to back.  Each plan keeps a 3m
+ * batch naming a plan twice goes through pobk_solve_host back to back.  The x pointers must be
+ * distinct (POBK_ERR_ARG otherwise, before anything runs).  Each plan keeps a 3m
  * staging buffer on the device.  Host buffers may be pageable; the overlap needs pinned memory.
  * Ordered after prior work on `stream`; blocks until reps are filled and x holds the solutions. */
 pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* const* f, double* const* x,

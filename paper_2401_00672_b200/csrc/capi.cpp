@@ -696,6 +696,10 @@ pobk_status pobk_solve_batch_host(pobk_plan_t* plans, int32_t nb, const double* 
     nl = ok ? 1 : 0;
   }
   if (nb < 2) nl = 0;
+  // the solutions come back concurrently: every system needs its own host x
+  for (int32_t b = 0; b < nb; b++)
+    for (int32_t c = 0; c < b; c++)
+      if (x[c] == x[b]) return fail(POBK_ERR_ARG, "x pointers must be distinct (systems " + std::to_string(c) + " and " + std::to_string(b) + ")");
   if (nl < 1) {  // back to back: each system through pobk_solve_host (copies, solve, copy back)
     for (int32_t b = 0; b < nb; b++) {
       pobk_status st = pobk_solve_host(plans[b], f[b], x[b], xstar ? xstar[b] : nullptr, opts, stream, reps ? reps + b : nullptr);

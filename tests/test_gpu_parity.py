@@ -568,6 +568,9 @@ def test_batch_host_equals_device_batch(env, nb, lanes):
                                             ctypes.cast(XS, ctypes.c_void_p), ctypes.byref(o), None,
                                             ctypes.cast((L.Report * nb)(), ctypes.c_void_p)))
     assert not any(b.any() for b in bad)
+    with pytest.raises(pk.PobkError):  # one host x for two systems
+        pk.solve_batch_host(plans[:2], hf[:2], [bad[0], bad[0]], hxs[:2], tol=0.2)
+    assert not bad[0].any()
     # a plan named twice: back to back through pobk_solve_host, each system its own result
     hx2 = [np.zeros(systems[0].m) for _ in range(2)]
     r2 = pk.solve_batch_host([plans[0], plans[0]], [hf[0], hf[0]], hx2, [hxs[0], hxs[0]], tol=0.2)
