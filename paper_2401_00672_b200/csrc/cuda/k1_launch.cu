@@ -11,6 +11,10 @@
 // The sweep loop is device-driven: the steps + the stop check are the body of a CUDA-graph WHILE
 // node whose condition the check kernel clears (no host round trip per sweep).  K1 is the
 // general fallback (any size, any thr); K2/K3 are the fast paths.
+//
+// K1E: the step and alpha kernels read a sliced-ELL copy of A~ (built on the device at the first
+// solve) in batches of 8 entries -- a step is a small grid of one-row threads, so the row's
+// dependent L2 round trips set its time (config 4: 678 -> 413 us/sweep); bitwise the CSR kernels.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -67,16 +71,166 @@ __global__ void __launch_bounds__(kNT) k1_scatter_ordered(const int32_t* __restr
   x[c] = xc;
 }
 
+// ---- K1E: the same two kernels on the sliced ELL copy (coalesced entry loads: with the CSR a
+// warp's 32 rows sit ~200 bytes apart, 32 sectors per load instruction).  Same operations in the
+// same order per row (common.cuh contract): bitwise the CSR kernels' iterates.
+// Loads in batches of kB entries (all columns, then all x~, then the products, then the ordered
+// adds): the row's ~2 x len dependent L2 round trips become ~2 x len / kB.
+constexpr int kB = 8;
+
+__device__ __forceinline__ double k1e_dot(const int32_t* __restrict__ ecol, const double* __restrict__ eval, int64_t b,
+                                          int len, const double* x) {
+  double sum = 0.0;
+  for (int j0 = 0; j0 < len; j0 += kB) {
+    int c[kB];
+    double v[kB], pr[kB];
+#pragma unroll
+    for (int u = 0; u < kB; u++) {
+      const bool on = j0 + u < len;
+      c[u] = on ? ecol[b + 32 * (int64_t)(j0 + u)] : -1;
+      v[u] = on ? eval[b + 32 * (int64_t)(j0 + u)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; u++) pr[u] = c[u] >= 0 ? x[c[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kB; u++) pr[u] = pin(__dmul_rn(v[u], pr[u]));
+#pragma unroll
+    for (int u = 0; u < kB; u++)
+      if (c[u] >= 0) sum = __dadd_rn(sum, pr[u]);
+  }
+  return sum;
+}
+
+__global__ void __launch_bounds__(kNT) k1e_step(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
+                                                const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                                const double* __restrict__ fs, const double* __restrict__ nrm2,
+                                                double* x, int s0, int s1, int slice0) {
+  const int s = s0 + blockIdx.x * kNT + threadIdx.x;
+  if (s >= s1) return;
+  const int len = rp[s + 1] - rp[s];
+  const int64_t b = sptr[slice0 + blockIdx.x * (kNT / 32) + (threadIdx.x >> 5)] + (threadIdx.x & 31);
+  const double alpha = __ddiv_rn(__dsub_rn(fs[s], k1e_dot(ecol, eval, b, len, x)), nrm2[s]);
+  // the row's columns are distinct (strictly increasing, validated), so a batch's x~ loads may
+  // all precede its stores
+  for (int j0 = 0; j0 < len; j0 += kB) {
+    int c[kB];
+    double v[kB], xv[kB];
+#pragma unroll
+    for (int u = 0; u < kB; u++) {
+      const bool on = j0 + u < len;
+      c[u] = on ? ecol[b + 32 * (int64_t)(j0 + u)] : -1;
+      v[u] = on ? eval[b + 32 * (int64_t)(j0 + u)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; u++) xv[u] = c[u] >= 0 ? x[c[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kB; u++)
+      if (c[u] >= 0) x[c[u]] = __dadd_rn(xv[u], __dmul_rn(alpha, v[u]));
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k1e_alpha(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
+                                                 const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                                 const double* __restrict__ fs, const double* __restrict__ nrm2,
+                                                 const double* __restrict__ x, double* __restrict__ alpha, int s0, int s1,
+                                                 int slice0) {
+  const int s = s0 + blockIdx.x * kNT + threadIdx.x;
+  if (s >= s1) return;
+  const int len = rp[s + 1] - rp[s];
+  const int64_t b = sptr[slice0 + blockIdx.x * (kNT / 32) + (threadIdx.x >> 5)] + (threadIdx.x & 31);
+  alpha[s - s0] = __ddiv_rn(__dsub_rn(fs[s], k1e_dot(ecol, eval, b, len, x)), nrm2[s]);
+}
+
+// one warp per slice: CSR rows -> the slice's interleaved entries (padding stays zero, never read)
+__global__ void __launch_bounds__(kNT) k1e_fill(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                const double* __restrict__ val, const int32_t* __restrict__ srow,
+                                                const int64_t* __restrict__ sptr, int32_t* __restrict__ ecol,
+                                                double* __restrict__ eval, int nslices) {
+  const int sl = blockIdx.x * (kNT / 32) + (threadIdx.x >> 5), l = threadIdx.x & 31;
+  if (sl >= nslices) return;
+  const int r = srow[2 * sl] + l;
+  if (r >= srow[2 * sl + 1]) return;
+  const int p0 = rp[r], len = rp[r + 1] - p0;
+  const int64_t b = sptr[sl] + l;
+  for (int j = 0; j < len; j++) {
+    ecol[b + 32 * (int64_t)j] = col[p0 + j];
+    eval[b + 32 * (int64_t)j] = val[p0 + j];
+  }
+}
+
+// Builds the sliced ELL copy (once per plan, before the graph capture).  Any failure (memory)
+// leaves k1e_col NULL: the CSR kernels run instead.  POBK_K1_CSR=1 keeps the CSR kernels.
+void build_k1e(Plan& p) {
+  if (p.k1e_col || getenv("POBK_K1_CSR") != nullptr || p.m == 0) return;
+  std::vector<int32_t> rp(p.m + 1), srow;
+  if (cudaMemcpy(rp.data(), p.A.rp, (p.m + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  std::vector<int64_t> sptr(1, 0);
+  std::vector<int32_t> slice0(p.nsteps, 0);
+  for (int k = 0; k < p.nsteps; k++) {
+    slice0[k] = (int32_t)(sptr.size() - 1);
+    for (int a = p.h_step_ptr[k]; a < p.h_step_ptr[k + 1]; a += 32) {
+      const int b = std::min(p.h_step_ptr[k + 1], a + 32);
+      int w = 0;
+      for (int r = a; r < b; r++) w = std::max(w, rp[r + 1] - rp[r]);
+      srow.push_back(a);
+      srow.push_back(b);
+      sptr.push_back(sptr.back() + 32 * (int64_t)w);
+    }
+  }
+  const int nsl = (int)(sptr.size() - 1);
+  const size_t ne = (size_t)std::max<int64_t>(sptr.back(), 1);
+  int32_t *ecol = nullptr, *d_srow = nullptr;
+  double* eval = nullptr;
+  int64_t* d_sptr = nullptr;
+  bool ok = cudaMalloc((void**)&ecol, ne * 4) == cudaSuccess && cudaMalloc((void**)&eval, ne * 8) == cudaSuccess &&
+            cudaMalloc((void**)&d_sptr, sptr.size() * 8) == cudaSuccess &&
+            cudaMalloc((void**)&d_srow, std::max<size_t>(srow.size(), 1) * 4) == cudaSuccess;
+  ok = ok && cudaMemset(ecol, 0, ne * 4) == cudaSuccess && cudaMemset(eval, 0, ne * 8) == cudaSuccess &&
+       cudaMemcpy(d_sptr, sptr.data(), sptr.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+       cudaMemcpy(d_srow, srow.data(), srow.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (ok && nsl > 0) {
+    k1e_fill<<<(nsl + kNT / 32 - 1) / (kNT / 32), kNT>>>(p.A.rp, p.A.col, p.A.val, d_srow, d_sptr, ecol, eval, nsl);
+    ok = cudaDeviceSynchronize() == cudaSuccess;
+  }
+  if (d_srow) cudaFree(d_srow);
+  if (!ok) {
+    cudaGetLastError();
+    if (ecol) cudaFree(ecol);
+    if (eval) cudaFree(eval);
+    if (d_sptr) cudaFree(d_sptr);
+    return;
+  }
+  p.allocations.push_back(ecol);
+  p.allocations.push_back(eval);
+  p.allocations.push_back(d_sptr);
+  p.k1e_col = ecol;
+  p.k1e_val = eval;
+  p.k1e_ptr = d_sptr;
+  p.h_k1e_slice0 = slice0;
+}
+
 cudaError_t capture_sweep(Plan& p, cudaStream_t cs, long long& nodes) {
   const bool atomic = getenv("POBK_THR_ATOMIC") != nullptr;  // the fp64-atomic scatter (order nondeterministic)
+  const bool ell = p.k1e_col != nullptr;
   for (int k = 0; k < p.nsteps; k++) {
     const int s0 = p.h_step_ptr[k], s1 = p.h_step_ptr[k + 1];
     const int grid = (s1 - s0 + kNT - 1) / kNT;
     if (!p.h_overlap[k]) {
-      k1_step<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, s0, s1);
+      if (ell)
+        k1e_step<<<grid, kNT, 0, cs>>>(p.A.rp, p.k1e_ptr, p.k1e_col, p.k1e_val, p.d_fs, p.A.nrm2, p.d_xt, s0, s1,
+                                       p.h_k1e_slice0[k]);
+      else
+        k1_step<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, s0, s1);
       nodes++;
     } else {
-      k1_alpha<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, p.d_alpha, s0, s1);
+      if (ell)
+        k1e_alpha<<<grid, kNT, 0, cs>>>(p.A.rp, p.k1e_ptr, p.k1e_col, p.k1e_val, p.d_fs, p.A.nrm2, p.d_xt, p.d_alpha, s0,
+                                        s1, p.h_k1e_slice0[k]);
+      else
+        k1_alpha<<<grid, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, p.d_alpha, s0, s1);
       nodes++;
       const int c0 = p.h_ov_colptr[k], c1 = p.h_ov_colptr[k + 1];
       if (atomic) {
@@ -224,6 +378,7 @@ cudaError_t build_graph_ordered(Plan& p) {
 
 cudaError_t build_graph(Plan& p) {
   cudaError_t e;
+  build_k1e(p);
   cudaGraph_t g;
   if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) return e;
   cudaGraphConditionalHandle h;

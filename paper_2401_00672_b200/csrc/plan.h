@@ -72,6 +72,12 @@ struct Plan {
   cudaGraph_t k1_graph = nullptr;
   cudaGraphExec_t k1_exec = nullptr;
   long long k1_nodes_per_sweep = 0;
+  // K1E: sliced ELL of A~ (32-row slices in schedule order, never across a step; entry j of the
+  // slice's row l at k1e_ptr[slice] + 32 j + l) so a warp's loads of row entries coalesce
+  int32_t* k1e_col = nullptr;
+  double* k1e_val = nullptr;
+  int64_t* k1e_ptr = nullptr;            // [nslices+1]
+  std::vector<int32_t> h_k1e_slice0;     // [nsteps] first slice of each step
   cudaGraph_t k1o_graph = nullptr;       // the residual-ordered sweep loop (opts.order)
   cudaGraphExec_t k1o_exec = nullptr;
   long long k1o_nodes_per_sweep = 0;
