@@ -13,8 +13,8 @@
 // general fallback (any size, any thr); K2/K3 are the fast paths.
 //
 // K1E: the step and alpha kernels read a sliced-ELL copy of A~ (built on the device at the first
-// solve) in batches of 8 entries -- a step is a small grid of one-row threads, so the row's
-// dependent L2 round trips set its time (config 4: 678 -> 413 us/sweep); bitwise the CSR kernels.
+// solve) in batches of 16 entries -- a step is a small grid of one-row threads, so the row's
+// dependent L2 round trips set its time (config 4: 678 -> 347 us/sweep); bitwise the CSR kernels.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kNT) k1_scatter_ordered(const int32_t* __restr
 // same order per row (common.cuh contract): bitwise the CSR kernels' iterates.
 // Loads in batches of kB entries (all columns, then all x~, then the products, then the ordered
 // adds): the row's ~2 x len dependent L2 round trips become ~2 x len / kB.
-constexpr int kB = 8;
+constexpr int kB = 16;
 
 __device__ __forceinline__ double k1e_dot(const int32_t* __restrict__ ecol, const double* __restrict__ eval, int64_t b,
                                           int len, const double* x) {
