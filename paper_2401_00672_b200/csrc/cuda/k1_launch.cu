@@ -101,10 +101,33 @@ __device__ __forceinline__ double k1e_dot(const int32_t* __restrict__ ecol, cons
   return sum;
 }
 
+__device__ __forceinline__ void k1e_row(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
+                                        const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                        const double* __restrict__ fs, const double* __restrict__ nrm2, double* x, int s0,
+                                        int s1, int slice0);
+
 __global__ void __launch_bounds__(kNT) k1e_step(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
                                                 const int32_t* __restrict__ ecol, const double* __restrict__ eval,
                                                 const double* __restrict__ fs, const double* __restrict__ nrm2,
                                                 double* x, int s0, int s1, int slice0) {
+  k1e_row(rp, sptr, ecol, eval, fs, nrm2, x, s0, s1, slice0);
+}
+
+// the residual-ordered loop's step (schedule position j of this sweep's order) on the same layout
+__global__ void __launch_bounds__(kNT) k1oe_step(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
+                                                 const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                                 const double* __restrict__ fs, const double* __restrict__ nrm2,
+                                                 double* x, const int32_t* __restrict__ step_ptr,
+                                                 const int32_t* __restrict__ slice0, const int32_t* __restrict__ order,
+                                                 int j) {
+  const int k = order[j];
+  k1e_row(rp, sptr, ecol, eval, fs, nrm2, x, step_ptr[k], step_ptr[k + 1], slice0[k]);
+}
+
+__device__ __forceinline__ void k1e_row(const int32_t* __restrict__ rp, const int64_t* __restrict__ sptr,
+                                        const int32_t* __restrict__ ecol, const double* __restrict__ eval,
+                                        const double* __restrict__ fs, const double* __restrict__ nrm2, double* x, int s0,
+                                        int s1, int slice0) {
   const int s = s0 + blockIdx.x * kNT + threadIdx.x;
   if (s >= s1) return;
   const int len = rp[s + 1] - rp[s];
@@ -185,7 +208,10 @@ void build_k1e(Plan& p) {
   int32_t *ecol = nullptr, *d_srow = nullptr;
   double* eval = nullptr;
   int64_t* d_sptr = nullptr;
+  int32_t* d_sl0 = nullptr;
   bool ok = cudaMalloc((void**)&ecol, ne * 4) == cudaSuccess && cudaMalloc((void**)&eval, ne * 8) == cudaSuccess &&
+            cudaMalloc((void**)&d_sl0, std::max<size_t>(slice0.size(), 1) * 4) == cudaSuccess &&
+            cudaMemcpy(d_sl0, slice0.data(), slice0.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
             cudaMalloc((void**)&d_sptr, sptr.size() * 8) == cudaSuccess &&
             cudaMalloc((void**)&d_srow, std::max<size_t>(srow.size(), 1) * 4) == cudaSuccess;
   ok = ok && cudaMemset(ecol, 0, ne * 4) == cudaSuccess && cudaMemset(eval, 0, ne * 8) == cudaSuccess &&
@@ -201,6 +227,7 @@ void build_k1e(Plan& p) {
     if (ecol) cudaFree(ecol);
     if (eval) cudaFree(eval);
     if (d_sptr) cudaFree(d_sptr);
+    if (d_sl0) cudaFree(d_sl0);
     return;
   }
   p.allocations.push_back(ecol);
@@ -209,6 +236,8 @@ void build_k1e(Plan& p) {
   p.k1e_col = ecol;
   p.k1e_val = eval;
   p.k1e_ptr = d_sptr;
+  p.allocations.push_back(d_sl0);
+  p.k1e_slice0 = d_sl0;
   p.h_k1e_slice0 = slice0;
 }
 
@@ -314,6 +343,7 @@ __global__ void __launch_bounds__(kNT) k1o_step(const int32_t* __restrict__ rp, 
 
 cudaError_t build_graph_ordered(Plan& p) {
   cudaError_t e;
+  build_k1e(p);
   // chunk list and per-step chunk ranges (host), scratch (device)
   std::vector<int32_t> cb, sc(p.nsteps + 1, 0);
   int32_t maxrows = 1;
@@ -357,8 +387,12 @@ cudaError_t build_graph_ordered(Plan& p) {
   k1o_order<<<1, 256, 0, cs>>>(d_sc, d_cs, d_cn, d_rho, d_order, p.nsteps);
   nodes += 3;
   for (int j = 0; j < p.nsteps; j++) {
-    k1o_step<<<(maxrows + kNT - 1) / kNT, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt, p.k3_step_ptr,
-                                                       d_order, j);
+    if (p.k1e_col)
+      k1oe_step<<<(maxrows + kNT - 1) / kNT, kNT, 0, cs>>>(p.A.rp, p.k1e_ptr, p.k1e_col, p.k1e_val, p.d_fs, p.A.nrm2,
+                                                          p.d_xt, p.k3_step_ptr, p.k1e_slice0, d_order, j);
+    else
+      k1o_step<<<(maxrows + kNT - 1) / kNT, kNT, 0, cs>>>(p.A.rp, p.A.col, p.A.val, p.d_fs, p.A.nrm2, p.d_xt,
+                                                         p.k3_step_ptr, d_order, j);
     nodes++;
   }
   e = cudaGetLastError();

@@ -78,6 +78,7 @@ struct Plan {
   double* k1e_val = nullptr;
   int64_t* k1e_ptr = nullptr;            // [nslices+1]
   std::vector<int32_t> h_k1e_slice0;     // [nsteps] first slice of each step
+  int32_t* k1e_slice0 = nullptr;         // device copy (the residual-ordered loop picks its step on the device)
   cudaGraph_t k1o_graph = nullptr;       // the residual-ordered sweep loop (opts.order)
   cudaGraphExec_t k1o_exec = nullptr;
   long long k1o_nodes_per_sweep = 0;
